@@ -1,0 +1,214 @@
+/*
+ * etree.h -- C ABI of the B200 E-Tree / E-Forest ADC library (libetree.so).
+ *
+ * Hot path of "Accelerated Distance Computation with Encoding Tree for High
+ * Dimensional Data" (arXiv 1509.05186).  Citations: P:n = PAPER.md line n,
+ * S:n = SPEC.md line n, A<n> = reading n in DESIGN.md §3.
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ * - Every call returns et_status (ET_OK = 0).  On error a thread-local message
+ *   is available from et_last_error().  Arguments are validated before any
+ *   launch; no output is written on a validation error.
+ * - Ownership: the CALLER owns every buffer passed in (host or device, as each
+ *   argument says).  The LIBRARY owns et_index (built by et_build_*, released
+ *   with et_index_free).  An index is immutable after build and may be queried
+ *   concurrently from different streams provided each call gets its own
+ *   workspace.
+ * - Query calls are asynchronous on `stream` (a cudaStream_t passed as void*;
+ *   NULL = legacy default stream) and never synchronise the host.  Build calls
+ *   are synchronous (they upload the index).
+ * - Layouts: vectors fp32 row-major [n][d]; codes uint8 row-major [n][M];
+ *   codebooks fp32 [M][K][d/M] (S:143 order); distance tables fp32 [Q][M][K];
+ *   distances are squared L2 (no sqrt).  K <= 256, d % M == 0.
+ * - Ids: int32.  A database vector is addressed by its SLOT (its row in the
+ *   codes array given to the build) and reported by its ID (ids[slot], or the
+ *   slot itself when ids == NULL).  Top-k orders by (distance, id) ascending
+ *   (A14); missing entries are (+inf, -1).
+ * - Device: every device pointer must live on the current CUDA device.
+ */
+#ifndef ETREE_H
+#define ETREE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum et_status {
+  ET_OK = 0,
+  ET_ERR_INSUFFICIENT_DATA = 1,   /* S:69   n < K                               */
+  ET_ERR_SUBSPACE_SPLIT = 2,      /* S:69   d % M != 0                          */
+  ET_ERR_INVALID_VECTOR = 3,      /* S:69   non-finite input                    */
+  ET_ERR_DIMENSION = 4,           /* S:79   length mismatch                     */
+  ET_ERR_INVALID_CODE = 5,        /* S:89   code byte >= K                      */
+  ET_ERR_CONFIG = 6,              /* S:119  parameter mismatch / bad split / k  */
+  ET_ERR_PRECONDITION = 7,        /* S:208  unsorted input etc.                 */
+  ET_ERR_EMPTY = 8,               /* S:208  N == 0                              */
+  ET_ERR_CORRUPT = 9,             /* S:218  malformed buffer                    */
+  ET_ERR_CUDA = 10,               /* a CUDA runtime error (message has it)      */
+  ET_ERR_OOM = 11,                /* device allocation failed                   */
+  ET_ERR_WORKSPACE = 12           /* workspace too small                        */
+} et_status;
+
+typedef struct et_index et_index;
+
+/* Per-tree statistics (§4.1).  For an IVF index the
+ * numbers are summed over all inverted lists. */
+typedef struct et_tree_stats {
+  int64_t N;               /* ids stored in this tree (4N bytes)                */
+  int32_t M;               /* code bytes (levels) of this tree                          */
+  int32_t layer0;          /* first code byte this tree covers (forests)                */
+  int64_t L1;              /* internal nodes                                            */
+  int64_t L2;              /* leaves = distinct (projected) codes                       */
+  int64_t total_postfix;   /* sum over leaves of M-1-depth                              */
+  int64_t lookups;         /* L1 + L2 + total_postfix = table lookups per query */
+  int64_t L2_records;      /* leaf records with the 7-bit n' <= 127 chaining (A9)       */
+  int64_t paper_bytes;     /* 4N + 2(L1 + L2_records) + chained postfix bytes   */
+  int64_t device_bytes;    /* bytes of this tree's device layout         */
+  int64_t groups;          /* id groups (leaves, or forest tuples) -- index-wide        */
+} et_tree_stats;
+
+const char* et_last_error(void);
+const char* et_version(void);
+
+/* ---------------------------------------------------------------------------
+ * PQ training and encoding (reading A15).  Not timed.
+ * ------------------------------------------------------------------------- */
+
+/* M independent k-means (k-means++ seeding from `seed`, then `lloyd_iters`
+ * Lloyd iterations; empty cluster -> farthest point; argmin ties -> lowest k).
+ * train: HOST fp32 [n][d].  codebooks: HOST fp32 [M][K][d/M] (written).
+ * objective_hist: optional HOST double [M][lloyd_iters] (objective after each
+ * assignment step; non-increasing).  Uses the current device for the
+ * assignment steps.  Errors: n < K, d % M, non-finite input, K > 256. */
+et_status et_build_codebooks(const float* train, int64_t n, int32_t d, int32_t M,
+                             int32_t K, int32_t lloyd_iters, uint64_t seed,
+                             float* codebooks, double* objective_hist);
+
+/* Encode: code byte m = argmin_k ||x_m - c_m(k)||^2, fp32 direct difference,
+ * ties -> lowest k.  codebooks, x: DEVICE; codes: DEVICE uint8 [n][M].
+ * centroids/assign optional (both DEVICE, may be NULL): if given, the residual
+ * x - centroids[assign[i]] is encoded (IVF). */
+et_status et_encode(const float* codebooks, int32_t d, int32_t M, int32_t K,
+                    const float* x, int64_t n, const float* centroids,
+                    const int32_t* assign, uint8_t* codes, void* stream);
+
+/* Nearest coarse centroid per vector (IVF list assignment; ties -> lower
+ * cell).  x: DEVICE [n][d]; centroids: DEVICE [nlist][d]; assign: DEVICE int32. */
+et_status et_assign(const float* centroids, int32_t nlist, int32_t d,
+                    const float* x, int64_t n, int32_t* assign, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Index build (Algorithm 1 semantics P:157-180, path compression P:153-154,
+ * chunked concatenation P:217-218).  Synchronous; inputs are HOST memory.
+ * ------------------------------------------------------------------------- */
+
+/* One E-Tree over all M bytes (M <= 8 on the GPU; deeper codes use a forest).
+ * codes: HOST uint8 [n][M].  ids: HOST int32 [n] or NULL (ids = slots).
+ * byte_perm: HOST int32 [M] or NULL (chunk order P:358-371; identity). */
+et_status et_build_etree(const uint8_t* codes, const int32_t* ids, int64_t n,
+                         int32_t M, int32_t K, const int32_t* byte_perm,
+                         et_index** out);
+
+/* E-Forest: T trees over the contiguous byte ranges split[t]..split[t+1]-1
+ * (A13); split: HOST int32 [T+1], split[0]=0, split[T]=M, each
+ * range 1..8 bytes.  T = 1 is the E-Tree. */
+et_status et_build_eforest(const uint8_t* codes, const int32_t* ids, int64_t n,
+                           int32_t M, int32_t K, const int32_t* byte_perm,
+                           int32_t T, const int32_t* split, et_index** out);
+
+/* Flat (uncompressed) layout of the same codes: one leaf per slot, LCP 0, so
+ * the scan performs naive ADC's N*M lookups (the comparison of P:376-377 on
+ * the same kernel).  M <= 8. */
+et_status et_build_flat(const uint8_t* codes, const int32_t* ids, int64_t n,
+                        int32_t M, int32_t K, et_index** out);
+
+/* IVF index: one E-Tree per inverted list.  codes: residual codes
+ * HOST [n][M]; list_of: HOST int32 [n] list of each vector (0..nlist-1);
+ * coarse: HOST fp32 [nlist][d] (uploaded; used for residual tables);
+ * codebooks: HOST fp32 [M][K][d/M] residual codebook (uploaded). */
+et_status et_build_ivf(const uint8_t* codes, const int32_t* ids, int64_t n,
+                       int32_t M, int32_t K, const int32_t* list_of,
+                       int32_t nlist, const float* coarse, int32_t d,
+                       const float* codebooks, et_index** out);
+
+et_status et_index_stats(const et_index* index, int32_t tree, et_tree_stats* out);
+/* Host-only: run the E-Tree/E-Forest build of et_build_eforest without a GPU
+ * and return the T per-tree statistics (out: HOST et_tree_stats [T]). */
+et_status et_build_stats(const uint8_t* codes, const int32_t* ids, int64_t n,
+                         int32_t M, int32_t K, const int32_t* byte_perm,
+                         int32_t T, const int32_t* split, et_tree_stats* out);
+/* trees in the index (T), groups, N, M, K */
+et_status et_index_info(const et_index* index, int32_t* T, int64_t* n,
+                        int32_t* M, int32_t* K, int64_t* groups, int32_t* nlist);
+void      et_index_free(et_index* index);
+
+/* ---------------------------------------------------------------------------
+ * Query path (the timed hot path).  All DEVICE pointers, async on `stream`.
+ * ------------------------------------------------------------------------- */
+
+/* Distance tables: luts[q][m][k] = sum_j (x_q[m*s+j] - C[m][k][j])^2
+ * in fp32, direct difference, j ascending (no GEMM expansion: DESIGN.md §5). */
+et_status et_compute_luts(const float* codebooks, int32_t d, int32_t M, int32_t K,
+                          const float* queries, int64_t Q, float* luts, void* stream);
+
+/* Bytes of device workspace et_etree_distances / et_etree_topk need. */
+et_status et_workspace_size(const et_index* index, int64_t Q, int32_t k,
+                            int32_t nprobe, size_t* bytes);
+
+/* Full output: out[q][slot] = ADC distance of database slot for
+ * query q, [Q][n].  Either `luts` ([Q][M][K]) or `queries` ([Q][d]) + the
+ * codebooks the index was built against must be given (queries => the tables
+ * are computed inside the scan kernel).  Not for IVF indexes. */
+et_status et_etree_distances(const et_index* index, const float* codebooks,
+                             int32_t d, const float* luts, const float* queries,
+                             int64_t Q, float* out, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* Fused top-k (north_star item 4): for each query the k smallest
+ * (distance, id) pairs; dist: DEVICE fp32 [Q][k]; ids: DEVICE int32 [Q][k].
+ * 1 <= k <= 256.  Tables as for et_etree_distances. */
+et_status et_etree_topk(const et_index* index, const float* codebooks, int32_t d,
+                        const float* luts, const float* queries, int64_t Q,
+                        int32_t k, float* dist, int32_t* ids, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* IVF search: probe the nprobe nearest coarse cells (fp32 direct difference,
+ * ties -> lower cell), residual tables per (query, cell), per-list E-Tree
+ * scan, fused top-k.  probes: optional DEVICE int32 [Q][nprobe] output. */
+et_status et_ivf_topk(const et_index* index, const float* queries, int64_t Q,
+                      int32_t nprobe, int32_t k, float* dist, int32_t* ids,
+                      int32_t* probes, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/* Merge G per-shard top-k lists (after an all-gather) into one:
+ * in_dist/in_ids: DEVICE [G][Q][k] (as gathered); out: DEVICE [Q][k].
+ * Order (distance, id); entries with id < 0 are empty. */
+et_status et_merge_topk(const float* in_dist, const int32_t* in_ids, int32_t G,
+                        int64_t Q, int32_t k, float* out_dist, int32_t* out_ids,
+                        void* stream);
+
+/* Naive ADC on the GPU (comparison kernel): out[q][slot] =
+ * sum_m luts[q][m][codes[slot][m]], m ascending.  codes DEVICE [n][M]. */
+et_status et_flat_adc(const float* luts, int64_t Q, int32_t M, int32_t K,
+                      const uint8_t* codes, int64_t n, float* out, void* stream);
+
+/* Number of kernel launches issued by this process (all entry points). */
+int64_t et_launch_count(void);
+
+/* Per-kernel timing (measurement support): when enabled, every launch issued
+ * by the query entry points is bracketed by CUDA events recorded on its own
+ * stream.  et_timing_get synchronises on the recorded events and returns the
+ * accumulated milliseconds and launch count of kernel `name` ("luts", "fill",
+ * "scan", "finalize", "gather"); returns 0 if that kernel never ran. */
+void et_timing_enable(int on);
+void et_timing_reset(void);
+int  et_timing_get(const char* name, double* total_ms, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ETREE_H */

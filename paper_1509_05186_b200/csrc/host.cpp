@@ -1,0 +1,1040 @@
+// host.cpp -- C ABI of libetree: argument checks, index build (sort, leaves,
+// groups, forest tuples, IVF lists, statistics), workspace planning and kernel
+// launches.  The build follows Algorithm 1's semantics: codes are
+// sorted lexicographically, identical codes share one leaf (A6), and the tree
+// is described by its leaves in depth-first order with each leaf's LCP to its
+// predecessor.  No code is shared with oracle/.
+#include "../../include/etree.h"
+#include "internal.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace et {
+
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+
+// ---------------------------------------------------------------------------
+// optional per-kernel timing: CUDA events recorded on the launching stream
+// around each launcher call (et_timing_enable); read back by et_timing_get.
+// ---------------------------------------------------------------------------
+static std::atomic<bool> g_timing{false};
+static std::mutex g_tmu;
+struct Pending { std::string name; cudaEvent_t a, b; };
+static std::vector<Pending> g_pending;
+static std::vector<cudaEvent_t> g_event_pool;
+static std::map<std::string, std::pair<double, long long>> g_tacc;
+
+static cudaEvent_t get_event() {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  if (!g_event_pool.empty()) { cudaEvent_t e = g_event_pool.back(); g_event_pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <class F>
+static cudaError_t timed(const char* name, cudaStream_t st, F f) {
+  if (!g_timing.load(std::memory_order_relaxed)) return f();
+  cudaEvent_t a = get_event(), b = get_event();
+  cudaEventRecord(a, st);
+  cudaError_t e = f();
+  cudaEventRecord(b, st);
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_pending.push_back({name, a, b});
+  return e;
+}
+
+static void drain_timing() {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  for (auto& p : g_pending) {
+    cudaEventSynchronize(p.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    auto& acc = g_tacc[p.name];
+    acc.first += ms;
+    acc.second += 1;
+    g_event_pool.push_back(p.a);
+    g_event_pool.push_back(p.b);
+  }
+  g_pending.clear();
+}
+
+static thread_local std::string g_err;
+static thread_local bool g_dry_run = false;   // build on the host only (et_build_stats)
+
+struct Error {
+  et_status st;
+  std::string msg;
+};
+
+[[noreturn]] static void fail(et_status st, const std::string& msg) { throw Error{st, msg}; }
+
+static void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) fail(ET_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(ET_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// device buffers owned by an index
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { if (p) cudaFree(p); }
+  template <class T>
+  void upload(const std::vector<T>& v) {
+    bytes = v.size() * sizeof(T);
+    if (bytes == 0 || g_dry_run) return;
+    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(index)");
+    cuda_check(cudaMemcpy(p, v.data(), bytes, cudaMemcpyHostToDevice), "upload(index)");
+  }
+  void upload_raw(const void* src, size_t n) {
+    bytes = n;
+    if (!n || g_dry_run) return;
+    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(index)");
+    cuda_check(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice), "upload(index)");
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+enum Kind { kTree = 0, kIvf = 1, kFlat = 2 };
+
+struct HostTree {
+  int MT = 0, layer0 = 0;
+  std::vector<uint64_t> code;   // packed little-endian, byte l at bits 8l
+  std::vector<uint8_t> lcp;
+  std::vector<uint64_t> mult;   // ids per leaf (stats)
+  et_tree_stats st{};
+};
+
+}  // namespace et
+
+struct et_index {
+  int kind = et::kTree;
+  int64_t N = 0;
+  int M = 0, K = 0, T = 1, d = 0, nlist = 0;
+  int split[et::kMaxTrees + 1] = {};
+  std::vector<int> layer_sub;
+  int64_t n_groups = 0;
+  int device = 0;
+  et_tree_stats stats[et::kMaxTrees] = {};
+  et::DevBuf code[et::kMaxTrees], lcp[et::kMaxTrees];
+  int64_t n_leaves[et::kMaxTrees] = {};
+  et::DevBuf group_off, ids, group_mult, group_minid, slot2group;
+  et::DevBuf t0_tup_off, tup_leaf[et::kMaxTrees];
+  et::DevBuf layer_sub_d;
+  et::DevBuf coarse, codebooks;      // IVF
+  std::vector<uint32_t> list_leaf_off;
+  et::DevBuf list_leaf_off_d;
+  double lookups_per_query = 0;      // sum over trees (+ tuples) -- planning
+};
+
+namespace et {
+
+// ---------------------------------------------------------------------------
+// sorting: stable LSD radix sort of slots by code bytes (lexicographic order)
+// ---------------------------------------------------------------------------
+// Returns the permutation of [0, n) that sorts rows of `codes` (row stride M,
+// using bytes [b0, b1)) lexicographically; equal rows keep slot order.
+static std::vector<uint32_t> sort_slots(const uint8_t* codes, int64_t n, int M, int b0, int b1,
+                                        const std::vector<uint32_t>* subset = nullptr) {
+  std::vector<uint32_t> a, b;
+  if (subset) a = *subset;
+  else { a.resize(n); std::iota(a.begin(), a.end(), 0u); }
+  b.resize(a.size());
+  std::vector<uint8_t> digit(a.size());
+  for (int l = b1 - 1; l >= b0; --l) {
+    size_t cnt[257] = {0};
+    for (size_t i = 0; i < a.size(); ++i) {
+      digit[i] = codes[(size_t)a[i] * M + l];
+      ++cnt[digit[i] + 1];
+    }
+    for (int v = 0; v < 256; ++v) cnt[v + 1] += cnt[v];
+    for (size_t i = 0; i < a.size(); ++i) b[cnt[digit[i]]++] = a[i];
+    a.swap(b);
+  }
+  return a;
+}
+
+static inline bool rows_equal(const uint8_t* codes, int M, uint32_t x, uint32_t y, int b0, int b1) {
+  return std::memcmp(codes + (size_t)x * M + b0, codes + (size_t)y * M + b0, b1 - b0) == 0;
+}
+
+static inline int row_lcp(const uint8_t* codes, int M, uint32_t x, uint32_t y, int b0, int b1) {
+  const uint8_t* a = codes + (size_t)x * M;
+  const uint8_t* b = codes + (size_t)y * M;
+  int l = 0;
+  while (b0 + l < b1 && a[b0 + l] == b[b0 + l]) ++l;
+  return l;
+}
+
+static inline uint64_t pack(const uint8_t* row, int b0, int b1) {
+  uint64_t v = 0;
+  for (int l = b0; l < b1; ++l) v |= (uint64_t)row[l] << (8 * (l - b0));
+  return v;
+}
+
+// Statistics of a tree given its leaves' LCP-with-predecessor and multiplicity
+// (plain definition): internal nodes at depth l = runs of
+// adjacent leaves sharing l+1 bytes => L1 = sum_i max(0, lcp_i - lcp_{i-1});
+// leaf depth = max(lcp_i, lcp_{i+1}); postfix = MT-1-depth.
+static void tree_stats(HostTree& t, int64_t N) {
+  const int64_t L2 = (int64_t)t.lcp.size();
+  int64_t L1 = 0, post = 0, recs = 0, post_recs = 0, look = 0;
+  for (int64_t i = 0; i < L2; ++i) {
+    const int li = (i == 0) ? 0 : t.lcp[i];
+    const int prev = (i <= 1) ? 0 : t.lcp[i - 1];
+    if (i >= 1) L1 += std::max(0, li - prev);
+    const int nxt = (i + 1 < L2) ? t.lcp[i + 1] : 0;
+    const int depth = std::min(t.MT - 1, std::max(li, nxt));
+    const int pf = t.MT - 1 - depth;
+    post += pf;
+    const int64_t r = ((int64_t)t.mult[i] + 126) / 127;
+    recs += r;
+    post_recs += r * pf;
+    look += t.MT - li;
+  }
+  if (L1 + L2 + post != look) fail(ET_ERR_CORRUPT, "internal: lookup identity violated");
+  t.st.N = N;
+  t.st.M = t.MT;
+  t.st.layer0 = t.layer0;
+  t.st.L1 = L1;
+  t.st.L2 = L2;
+  t.st.total_postfix = post;
+  t.st.lookups = look;
+  t.st.L2_records = recs;
+  t.st.paper_bytes = 4 * N + 2 * (L1 + recs) + post_recs;
+  t.st.device_bytes = L2 * 9;
+}
+
+static void check_codes(const uint8_t* codes, int64_t n, int M, int K) {
+  if (K < 256) {
+    for (int64_t i = 0; i < n * M; ++i)
+      if (codes[i] >= K) fail(ET_ERR_INVALID_CODE, "code byte >= K");
+  }
+}
+
+// groups (distinct full codes in sorted order) + ids, from a sorted slot list
+struct Groups {
+  std::vector<uint32_t> off;      // [G+1]
+  std::vector<int32_t> ids;       // ascending within a group
+  std::vector<uint32_t> first;    // representative slot of each group
+};
+
+static Groups make_groups(const uint8_t* codes, int M, const std::vector<uint32_t>& order,
+                          const int32_t* ids, int b0, int b1) {
+  Groups g;
+  const size_t n = order.size();
+  g.ids.resize(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (i == 0 || !rows_equal(codes, M, order[i - 1], order[i], b0, b1)) {
+      g.off.push_back((uint32_t)i);
+      g.first.push_back(order[i]);
+    }
+    g.ids[i] = ids ? ids[order[i]] : (int32_t)order[i];
+  }
+  g.off.push_back((uint32_t)n);
+  if (ids) {
+    for (size_t j = 0; j + 1 < g.off.size(); ++j) std::sort(g.ids.begin() + g.off[j], g.ids.begin() + g.off[j + 1]);
+  }
+  return g;
+}
+
+static void upload_groups(et_index* ix, const Groups& g, const std::vector<uint32_t>& slot2group) {
+  const size_t G = g.off.size() - 1;
+  std::vector<uint32_t> mult(G);
+  std::vector<int32_t> minid(G);
+  for (size_t j = 0; j < G; ++j) {
+    mult[j] = g.off[j + 1] - g.off[j];
+    minid[j] = g.ids[g.off[j]];
+  }
+  ix->n_groups = (int64_t)G;
+  ix->group_off.upload(g.off);
+  ix->ids.upload(g.ids);
+  ix->group_mult.upload(mult);
+  ix->group_minid.upload(minid);
+  if (!slot2group.empty()) ix->slot2group.upload(slot2group);
+}
+
+static void finish_tree(et_index* ix, int t, HostTree& h) {
+  ix->n_leaves[t] = (int64_t)h.code.size();
+  ix->code[t].upload(h.code);
+  ix->lcp[t].upload(h.lcp);
+  ix->stats[t] = h.st;
+}
+
+static void set_layers(et_index* ix, const int32_t* byte_perm) {
+  ix->layer_sub.resize(ix->M);
+  for (int l = 0; l < ix->M; ++l) ix->layer_sub[l] = byte_perm ? byte_perm[l] : l;
+  if (byte_perm) {
+    std::vector<int> seen(ix->M, 0);
+    for (int l = 0; l < ix->M; ++l) {
+      if (byte_perm[l] < 0 || byte_perm[l] >= ix->M || seen[byte_perm[l]]++) fail(ET_ERR_CONFIG, "invalid byte permutation");
+    }
+  }
+  ix->layer_sub_d.upload(ix->layer_sub);
+}
+
+// codes permuted so that byte l of the stored code is original byte perm[l]
+static std::vector<uint8_t> permute_codes(const uint8_t* codes, int64_t n, int M, const int32_t* perm) {
+  std::vector<uint8_t> out((size_t)n * M);
+  for (int64_t i = 0; i < n; ++i)
+    for (int l = 0; l < M; ++l) out[(size_t)i * M + l] = codes[(size_t)i * M + (perm ? perm[l] : l)];
+  return out;
+}
+
+static void check_ids(const int32_t* ids, int64_t n) {
+  if (!ids) return;
+  for (int64_t i = 0; i < n; ++i)
+    if (ids[i] < 0) fail(ET_ERR_CONFIG, "ids must be non-negative");
+}
+
+// E-Forest / E-Tree build (T = 1 is the E-Tree).
+static et_index* build_forest(const uint8_t* codes_in, const int32_t* ids, int64_t n, int M, int K,
+                              const int32_t* byte_perm, int T, const int32_t* split) {
+  if (n <= 0) fail(ET_ERR_EMPTY, "empty dataset");
+  if (n > INT32_MAX) fail(ET_ERR_CONFIG, "n exceeds int32 ids");
+  if (M <= 0 || K <= 0 || K > 256) fail(ET_ERR_CONFIG, "need 1 <= K <= 256 and M >= 1");
+  if (T < 1 || T > kMaxTrees) fail(ET_ERR_CONFIG, "T must be 1..4");
+  if (split[0] != 0 || split[T] != M) fail(ET_ERR_CONFIG, "split must start at 0 and end at M");
+  for (int t = 0; t < T; ++t) {
+    const int w = split[t + 1] - split[t];
+    if (w < 1 || w > kMaxMT) fail(ET_ERR_CONFIG, "each tree must cover 1..8 code bytes (use a forest for M > 8)");
+  }
+  check_codes(codes_in, n, M, K);
+  check_ids(ids, n);
+  std::unique_ptr<et_index> ix(new et_index);
+  ix->kind = kTree;
+  ix->N = n; ix->M = M; ix->K = K; ix->T = T;
+  for (int t = 0; t <= T; ++t) ix->split[t] = split[t];
+  if (!g_dry_run) cudaGetDevice(&ix->device);
+  set_layers(ix.get(), byte_perm);
+  std::vector<uint8_t> pc = permute_codes(codes_in, n, M, byte_perm);
+  const uint8_t* codes = pc.data();
+
+  // full-code sort -> groups (distinct full codes, in lexicographic order)
+  std::vector<uint32_t> order = sort_slots(codes, n, M, 0, M);
+  Groups g = make_groups(codes, M, order, ids, 0, M);
+  const size_t G = g.off.size() - 1;
+  std::vector<uint32_t> slot2group(n);
+  for (size_t j = 0; j < G; ++j)
+    for (uint32_t i = g.off[j]; i < g.off[j + 1]; ++i) slot2group[order[i]] = (uint32_t)j;
+  upload_groups(ix.get(), g, slot2group);
+
+  double look = 0;
+  // tree 0: groups sorted by full code are sorted by the tree-0 projection too
+  {
+    HostTree h;
+    h.MT = split[1]; h.layer0 = 0;
+    std::vector<uint32_t> tup_off;
+    for (size_t j = 0; j < G; ++j) {
+      const uint32_t r = g.first[j];
+      const bool newleaf = (j == 0) || !rows_equal(codes, M, g.first[j - 1], r, 0, split[1]);
+      if (newleaf) {
+        h.code.push_back(pack(codes + (size_t)r * M, 0, split[1]));
+        h.lcp.push_back(j == 0 ? 0 : (uint8_t)row_lcp(codes, M, g.first[j - 1], r, 0, split[1]));
+        h.mult.push_back(0);
+        tup_off.push_back((uint32_t)j);
+      }
+      h.mult.back() += g.off[j + 1] - g.off[j];
+    }
+    tup_off.push_back((uint32_t)G);
+    tree_stats(h, n);
+    look += (double)h.st.lookups;
+    finish_tree(ix.get(), 0, h);
+    if (T > 1) {
+      ix->t0_tup_off.upload(tup_off);
+      look += (double)G;   // one join per tuple
+    }
+  }
+  // trees 1..T-1: distinct projections, sorted; tuple -> leaf
+  for (int t = 1; t < T; ++t) {
+    const int b0 = split[t], b1 = split[t + 1];
+    std::vector<uint32_t> reps(g.first.begin(), g.first.end());
+    std::vector<uint32_t> so = sort_slots(codes, n, M, b0, b1, &reps);
+    // group id of each rep (rep -> position in g.first): use slot2group
+    HostTree h;
+    h.MT = b1 - b0; h.layer0 = b0;
+    std::vector<uint32_t> tup_leaf(G);
+    for (size_t i = 0; i < so.size(); ++i) {
+      const uint32_t r = so[i];
+      const bool newleaf = (i == 0) || !rows_equal(codes, M, so[i - 1], r, b0, b1);
+      if (newleaf) {
+        h.code.push_back(pack(codes + (size_t)r * M, b0, b1));
+        h.lcp.push_back(i == 0 ? 0 : (uint8_t)row_lcp(codes, M, so[i - 1], r, b0, b1));
+        h.mult.push_back(0);
+      }
+      const uint32_t grp = slot2group[r];
+      tup_leaf[grp] = (uint32_t)(h.code.size() - 1);
+      h.mult.back() += g.off[grp + 1] - g.off[grp];
+    }
+    tree_stats(h, n);
+    look += (double)h.st.lookups;
+    finish_tree(ix.get(), t, h);
+    ix->tup_leaf[t].upload(tup_leaf);
+  }
+  for (int t = 0; t < T; ++t) ix->stats[t].groups = (int64_t)G;
+  ix->lookups_per_query = look;
+  return ix.release();
+}
+
+static et_index* build_flat(const uint8_t* codes, const int32_t* ids, int64_t n, int M, int K) {
+  if (n <= 0) fail(ET_ERR_EMPTY, "empty dataset");
+  if (M < 1 || M > kMaxMT) fail(ET_ERR_CONFIG, "flat index: 1 <= M <= 8");
+  if (K <= 0 || K > 256) fail(ET_ERR_CONFIG, "K must be 1..256");
+  check_codes(codes, n, M, K);
+  check_ids(ids, n);
+  std::unique_ptr<et_index> ix(new et_index);
+  ix->kind = kFlat;
+  ix->N = n; ix->M = M; ix->K = K; ix->T = 1;
+  ix->split[0] = 0; ix->split[1] = M;
+  cudaGetDevice(&ix->device);
+  set_layers(ix.get(), nullptr);
+  HostTree h;
+  h.MT = M;
+  h.code.resize(n);
+  h.lcp.assign(n, 0);
+  h.mult.assign(n, 1);
+  for (int64_t i = 0; i < n; ++i) h.code[i] = pack(codes + (size_t)i * M, 0, M);
+  h.st.N = n; h.st.M = M; h.st.L2 = n; h.st.lookups = n * M; h.st.device_bytes = n * 9;
+  h.st.L2_records = n; h.st.total_postfix = n * (M - 1); h.st.paper_bytes = 4 * n + n * M;
+  finish_tree(ix.get(), 0, h);
+  Groups g;
+  g.off.resize(n + 1);
+  g.ids.resize(n);
+  for (int64_t i = 0; i <= n; ++i) g.off[i] = (uint32_t)i;
+  for (int64_t i = 0; i < n; ++i) g.ids[i] = ids ? ids[i] : (int32_t)i;
+  std::vector<uint32_t> s2g(n);
+  std::iota(s2g.begin(), s2g.end(), 0u);
+  upload_groups(ix.get(), g, s2g);
+  ix->stats[0].groups = n;
+  ix->lookups_per_query = (double)n * M;
+  return ix.release();
+}
+
+static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t n, int M, int K,
+                           const int32_t* list_of, int nlist, const float* coarse, int d,
+                           const float* codebooks) {
+  if (n <= 0) fail(ET_ERR_EMPTY, "empty dataset");
+  if (M < 1 || M > kMaxMT) fail(ET_ERR_CONFIG, "IVF lists: 1 <= M <= 8");
+  if (K <= 0 || K > 256) fail(ET_ERR_CONFIG, "K must be 1..256");
+  if (nlist < 1) fail(ET_ERR_CONFIG, "nlist >= 1");
+  if (d <= 0 || d % M) fail(ET_ERR_SUBSPACE_SPLIT, "d % M != 0");
+  check_codes(codes_in, n, M, K);
+  check_ids(ids, n);
+  for (int64_t i = 0; i < n; ++i)
+    if (list_of[i] < 0 || list_of[i] >= nlist) fail(ET_ERR_CONFIG, "list_of out of range");
+  std::unique_ptr<et_index> ix(new et_index);
+  ix->kind = kIvf;
+  ix->N = n; ix->M = M; ix->K = K; ix->T = 1; ix->d = d; ix->nlist = nlist;
+  ix->split[0] = 0; ix->split[1] = M;
+  cudaGetDevice(&ix->device);
+  set_layers(ix.get(), nullptr);
+  // bucket slots by list (stable), then sort each list by code
+  std::vector<std::vector<uint32_t>> members(nlist);
+  for (int64_t i = 0; i < n; ++i) members[list_of[i]].push_back((uint32_t)i);
+  HostTree h;
+  h.MT = M;
+  Groups g;
+  std::vector<uint32_t> s2g(n);
+  ix->list_leaf_off.assign(nlist + 1, 0);
+  et_tree_stats tot{};
+  for (int c = 0; c < nlist; ++c) {
+    ix->list_leaf_off[c] = (uint32_t)h.code.size();
+    if (members[c].empty()) continue;
+    std::vector<uint32_t> so = sort_slots(codes_in, n, M, 0, M, &members[c]);
+    HostTree lt;
+    lt.MT = M;
+    for (size_t i = 0; i < so.size(); ++i) {
+      const uint32_t r = so[i];
+      const bool newleaf = (i == 0) || !rows_equal(codes_in, M, so[i - 1], r, 0, M);
+      if (newleaf) {
+        const uint64_t pk = pack(codes_in + (size_t)r * M, 0, M);
+        const uint8_t lp = i == 0 ? 0 : (uint8_t)row_lcp(codes_in, M, so[i - 1], r, 0, M);
+        lt.code.push_back(pk); lt.lcp.push_back(lp); lt.mult.push_back(0);
+        h.code.push_back(pk); h.lcp.push_back(lp);
+        g.off.push_back((uint32_t)g.ids.size());
+        g.first.push_back(r);
+      }
+      lt.mult.back() += 1;
+      s2g[r] = (uint32_t)(h.code.size() - 1);
+      g.ids.push_back(ids ? ids[r] : (int32_t)r);
+    }
+    tree_stats(lt, (int64_t)so.size());
+    tot.L1 += lt.st.L1; tot.L2 += lt.st.L2; tot.total_postfix += lt.st.total_postfix;
+    tot.lookups += lt.st.lookups; tot.L2_records += lt.st.L2_records; tot.paper_bytes += lt.st.paper_bytes;
+  }
+  ix->list_leaf_off[nlist] = (uint32_t)h.code.size();
+  g.off.push_back((uint32_t)g.ids.size());
+  if (ids) {
+    for (size_t j = 0; j + 1 < g.off.size(); ++j) std::sort(g.ids.begin() + g.off[j], g.ids.begin() + g.off[j + 1]);
+  }
+  upload_groups(ix.get(), g, s2g);
+  tot.N = n; tot.M = M; tot.device_bytes = (int64_t)h.code.size() * 9;
+  tot.groups = (int64_t)(g.off.size() - 1);
+  ix->n_leaves[0] = (int64_t)h.code.size();
+  ix->code[0].upload(h.code);
+  ix->lcp[0].upload(h.lcp);
+  ix->stats[0] = tot;
+  ix->list_leaf_off_d.upload(ix->list_leaf_off);
+  ix->coarse.upload_raw(coarse, (size_t)nlist * d * 4);
+  ix->codebooks.upload_raw(codebooks, (size_t)M * K * (d / M) * 4);
+  ix->lookups_per_query = (double)tot.lookups / std::max(1, nlist);
+  return ix.release();
+}
+
+// ---------------------------------------------------------------------------
+// query planning
+// ---------------------------------------------------------------------------
+static int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && cached[dev]) return cached[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev < 64) cached[dev] = n;
+  return n;
+}
+
+struct Plan {
+  int n_chunks = 0, S = 1, n_units = 0, MTmax = 0, B = 0;
+  bool lut0 = false;
+  int64_t part_stride = 0;
+  int64_t part_base[kMaxTrees] = {};
+};
+
+static int topk_B(int k) { return ((2 * k + 64 + 31) / 32) * 32; }
+
+static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
+  Plan pl;
+  for (int t = 0; t < ix->T; ++t) pl.MTmax = std::max(pl.MTmax, ix->stats[t].M);
+  pl.lut0 = (pl.MTmax == 8);
+  const int64_t base = (Q + 31) / 32;
+  // Cost model per unit (cycles of one SM): tables ~ nq * K * d * 2 / 128 * 1.25
+  // (fp32 lanes), scan ~ 1.5 * lookups per query / S (one warp-wide smem lookup
+  // per lookup for 32 queries).  Pick the (chunks, S) with the least makespan.
+  const double K = ix->K;
+  const double d = std::max(1, ix->kind == kIvf ? ix->d : ix->M * 16);
+  const double look = std::max(1.0, ix->lookups_per_query);
+  double best = 1e300;
+  const int64_t cand_chunks[2] = {base, std::min<int64_t>(Q, ((base + nsm - 1) / nsm) * nsm)};
+  const int smax = (ix->T > 1) ? 1 : 64;
+  for (int ci = 0; ci < 2; ++ci) {
+    const int64_t nc = std::max<int64_t>(1, cand_chunks[ci]);
+    const double nq = std::min<double>(32.0, std::ceil((double)Q / nc));
+    for (int S = 1; S <= smax; S *= 2) {
+      const int64_t units = nc * S;
+      if (units > (1 << 30)) break;
+      const double per = nq * K * d * 2.0 / 128.0 * 1.25 + 1.5 * look / S + 2000.0;
+      const double waves = std::ceil((double)units / nsm);
+      const double cost = waves * per;
+      if (cost < best * 0.98) { best = cost; pl.n_chunks = (int)nc; pl.S = S; }
+    }
+  }
+  pl.n_units = pl.n_chunks * pl.S;
+  pl.B = topk_B(std::max(1, k));
+  int64_t off = 0;
+  for (int t = 1; t < ix->T; ++t) { pl.part_base[t] = off; off += ix->n_leaves[t] * 32; }
+  pl.part_stride = off;
+  return pl;
+}
+
+struct Carve {
+  char* base;
+  size_t off = 0, cap;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+struct Work {
+  int* chunk_q; int* qslot_off; int* qslot;
+  float* lut0; float* partials; float* leafdist;
+  uint2* cand; int* cand_cnt; float* unit_thr;
+};
+
+static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool full, int slots_per_q) {
+  Work w{};
+  w.chunk_q = c.take<int>((size_t)pl.n_chunks * 32);
+  w.qslot_off = c.take<int>(Q + 1);
+  w.qslot = c.take<int>((size_t)Q * slots_per_q);
+  w.lut0 = pl.lut0 ? c.take<float>((size_t)pl.n_units * 256 * 32) : nullptr;
+  w.partials = pl.part_stride ? c.take<float>((size_t)pl.n_units * pl.part_stride) : nullptr;
+  if (full) {
+    w.leafdist = c.take<float>((size_t)pl.n_chunks * ix->n_groups * 32);
+  } else {
+    w.cand = c.take<uint2>((size_t)pl.n_units * kWarps * 32 * pl.B);
+    w.cand_cnt = c.take<int>((size_t)pl.n_units * kWarps * 32);
+    w.unit_thr = c.take<float>((size_t)pl.n_units * 32);
+  }
+  return w;
+}
+
+static size_t ws_bytes(const et_index* ix, const Plan& pl, int64_t Q, bool full, int slots_per_q) {
+  Carve c{nullptr, 0, 0};
+  carve(c, ix, pl, Q, full, slots_per_q);
+  return c.off + 256;
+}
+
+static void fill_scan_common(ScanParams& sp, const et_index* ix, const Plan& pl) {
+  sp.M = ix->M; sp.K = ix->K;
+  sp.layer_sub = ix->layer_sub_d.as<int>();
+  sp.T = ix->T;
+  for (int t = 0; t < ix->T; ++t) {
+    sp.tree[t].MT = ix->stats[t].M;
+    sp.tree[t].layer0 = ix->split[t];
+    sp.tree[t].n_leaves = ix->n_leaves[t];
+    sp.tree[t].code = ix->code[t].as<uint64_t>();
+    sp.tree[t].lcp = ix->lcp[t].as<uint8_t>();
+    sp.tup_leaf[t] = ix->tup_leaf[t].as<uint32_t>();
+    sp.part_base[t] = pl.part_base[t];
+  }
+  sp.t0_tup_off = ix->t0_tup_off.as<uint32_t>();
+  sp.group_mult = ix->group_mult.as<uint32_t>();
+  sp.group_minid = ix->group_minid.as<int32_t>();
+  sp.n_groups = ix->n_groups;
+  sp.part_stride = pl.part_stride;
+  sp.n_units = pl.n_units;
+  sp.S = pl.S;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// tables source check shared by distances/topk
+static void table_source(ScanParams& sp, const et_index* ix, const float* codebooks, int d,
+                         const float* luts, const float* queries) {
+  if (luts) {
+    sp.luts = luts;
+  } else {
+    if (!queries || !codebooks) fail(ET_ERR_CONFIG, "need either luts or (queries and codebooks)");
+    if (d <= 0 || d % ix->M) fail(ET_ERR_SUBSPACE_SPLIT, "d % M != 0");
+    sp.queries = queries;
+    sp.codebooks = codebooks;
+    sp.d = d;
+    sp.s = d / ix->M;
+    sp.vec4 = aligned16(queries) && aligned16(codebooks) && (d % 4 == 0) ? 1 : 0;
+  }
+}
+
+}  // namespace et
+
+using namespace et;
+
+#define ET_API_BEGIN try {
+#define ET_API_END                                              \
+  }                                                             \
+  catch (const Error& e) {                                      \
+    g_err = e.msg;                                              \
+    return e.st;                                                \
+  }                                                             \
+  catch (const std::bad_alloc&) {                               \
+    g_err = "host allocation failed";                           \
+    return ET_ERR_OOM;                                          \
+  }                                                             \
+  catch (const std::exception& e) {                             \
+    g_err = e.what();                                           \
+    return ET_ERR_CONFIG;                                       \
+  }                                                             \
+  g_err.clear();                                                \
+  return ET_OK;
+
+extern "C" {
+
+const char* et_last_error(void) { return g_err.c_str(); }
+
+void et_timing_enable(int on) {
+  if (!on) drain_timing();
+  g_timing.store(on != 0);
+}
+
+void et_timing_reset(void) {
+  drain_timing();
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_tacc.clear();
+}
+
+int et_timing_get(const char* name, double* total_ms, int64_t* count) {
+  drain_timing();
+  std::lock_guard<std::mutex> lk(g_tmu);
+  auto it = g_tacc.find(name);
+  if (it == g_tacc.end()) { if (total_ms) *total_ms = 0; if (count) *count = 0; return 0; }
+  if (total_ms) *total_ms = it->second.first;
+  if (count) *count = it->second.second;
+  return 1;
+}
+const char* et_version(void) { return "etree-b200 0.1 (sm_100a)"; }
+int64_t et_launch_count(void) { return (int64_t)g_launches.load(); }
+
+et_status et_build_etree(const uint8_t* codes, const int32_t* ids, int64_t n, int32_t M, int32_t K,
+                         const int32_t* byte_perm, et_index** out) {
+  ET_API_BEGIN
+  if (!codes || !out) fail(ET_ERR_CONFIG, "null argument");
+  if (M > kMaxMT) fail(ET_ERR_CONFIG, "a single E-Tree supports M <= 8 on the GPU; build a forest");
+  int32_t split[2] = {0, M};
+  *out = build_forest(codes, ids, n, M, K, byte_perm, 1, split);
+  ET_API_END
+}
+
+et_status et_build_eforest(const uint8_t* codes, const int32_t* ids, int64_t n, int32_t M, int32_t K,
+                           const int32_t* byte_perm, int32_t T, const int32_t* split, et_index** out) {
+  ET_API_BEGIN
+  if (!codes || !out || !split) fail(ET_ERR_CONFIG, "null argument");
+  *out = build_forest(codes, ids, n, M, K, byte_perm, T, split);
+  ET_API_END
+}
+
+et_status et_build_flat(const uint8_t* codes, const int32_t* ids, int64_t n, int32_t M, int32_t K,
+                        et_index** out) {
+  ET_API_BEGIN
+  if (!codes || !out) fail(ET_ERR_CONFIG, "null argument");
+  *out = build_flat(codes, ids, n, M, K);
+  ET_API_END
+}
+
+et_status et_build_ivf(const uint8_t* codes, const int32_t* ids, int64_t n, int32_t M, int32_t K,
+                       const int32_t* list_of, int32_t nlist, const float* coarse, int32_t d,
+                       const float* codebooks, et_index** out) {
+  ET_API_BEGIN
+  if (!codes || !out || !list_of || !coarse || !codebooks) fail(ET_ERR_CONFIG, "null argument");
+  *out = build_ivf(codes, ids, n, M, K, list_of, nlist, coarse, d, codebooks);
+  ET_API_END
+}
+
+et_status et_build_stats(const uint8_t* codes, const int32_t* ids, int64_t n, int32_t M, int32_t K,
+                         const int32_t* byte_perm, int32_t T, const int32_t* split, et_tree_stats* out) {
+  ET_API_BEGIN
+  if (!codes || !out || !split) fail(ET_ERR_CONFIG, "null argument");
+  struct Dry { Dry() { g_dry_run = true; } ~Dry() { g_dry_run = false; } } dry;
+  std::unique_ptr<et_index> ix(build_forest(codes, ids, n, M, K, byte_perm, T, split));
+  for (int t = 0; t < T; ++t) out[t] = ix->stats[t];
+  ET_API_END
+}
+
+et_status et_index_stats(const et_index* ix, int32_t tree, et_tree_stats* out) {
+  ET_API_BEGIN
+  if (!ix || !out) fail(ET_ERR_CONFIG, "null argument");
+  if (tree < 0 || tree >= ix->T) fail(ET_ERR_CONFIG, "tree index out of range");
+  *out = ix->stats[tree];
+  ET_API_END
+}
+
+et_status et_index_info(const et_index* ix, int32_t* T, int64_t* n, int32_t* M, int32_t* K, int64_t* groups,
+                        int32_t* nlist) {
+  ET_API_BEGIN
+  if (!ix) fail(ET_ERR_CONFIG, "null index");
+  if (T) *T = ix->T;
+  if (n) *n = ix->N;
+  if (M) *M = ix->M;
+  if (K) *K = ix->K;
+  if (groups) *groups = ix->n_groups;
+  if (nlist) *nlist = ix->nlist;
+  ET_API_END
+}
+
+void et_index_free(et_index* ix) { delete ix; }
+
+et_status et_compute_luts(const float* codebooks, int32_t d, int32_t M, int32_t K, const float* queries,
+                          int64_t Q, float* luts, void* stream) {
+  ET_API_BEGIN
+  if (M <= 0 || K <= 0 || K > 256) fail(ET_ERR_CONFIG, "bad M/K");
+  if (d <= 0 || d % M) fail(ET_ERR_SUBSPACE_SPLIT, "d % M != 0");
+  if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
+  if (Q == 0) { g_err.clear(); return ET_OK; }
+  if (!codebooks || !queries || !luts) fail(ET_ERR_CONFIG, "null argument");
+  const bool v4 = aligned16(codebooks) && aligned16(queries);
+  cudaStream_t st = (cudaStream_t)stream;
+  cuda_check(timed("luts", st, [&] { return launch_luts(codebooks, d, M, K, queries, Q, luts, v4, st); }), "compute_luts");
+  ET_API_END
+}
+
+et_status et_workspace_size(const et_index* ix, int64_t Q, int32_t k, int32_t nprobe, size_t* bytes) {
+  ET_API_BEGIN
+  if (!ix || !bytes) fail(ET_ERR_CONFIG, "null argument");
+  if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
+  const int nsm = num_sms();
+  if (ix->kind == kIvf) fail(ET_ERR_CONFIG, "IVF workspace: use et_ivf_workspace_size");
+  const bool full = (k <= 0);
+  Plan pl = make_plan(ix, std::max<int64_t>(Q, 1), full ? 1 : k, nsm);
+  *bytes = ws_bytes(ix, pl, std::max<int64_t>(Q, 1), full, 1);
+  (void)nprobe;
+  ET_API_END
+}
+
+et_status et_etree_distances(const et_index* ix, const float* codebooks, int32_t d, const float* luts,
+                             const float* queries, int64_t Q, float* out, void* workspace, size_t ws,
+                             void* stream) {
+  ET_API_BEGIN
+  if (!ix || !out) fail(ET_ERR_CONFIG, "null argument");
+  if (ix->kind == kIvf) fail(ET_ERR_CONFIG, "full output is not defined for IVF indexes");
+  if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
+  if (Q == 0) { g_err.clear(); return ET_OK; }
+  ScanParams sp;
+  table_source(sp, ix, codebooks, d, luts, queries);
+  const int nsm = num_sms();
+  Plan pl = make_plan(ix, Q, 1, nsm);
+  pl.S = 1;   // full output: one unit per chunk writes every group
+  pl.n_units = pl.n_chunks;
+  const size_t need = ws_bytes(ix, pl, Q, true, 1);
+  if (!workspace || ws < need) fail(ET_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  Carve c{reinterpret_cast<char*>(workspace), 0, ws};
+  Work w = carve(c, ix, pl, Q, true, 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  cuda_check(timed("fill", st, [&] { return launch_fill_flat(Q, pl.n_chunks, w.chunk_q, w.qslot_off, w.qslot, st); }), "fill");
+  fill_scan_common(sp, ix, pl);
+  sp.chunk_q = w.chunk_q;
+  sp.lut0 = w.lut0;
+  sp.partials = w.partials;
+  sp.mode = kModeFull;
+  sp.leafdist = w.leafdist;
+  cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(full)");
+  cuda_check(timed("gather", st, [&] {
+               return launch_gather_full(w.leafdist, ix->slot2group.as<uint32_t>(), ix->n_groups, ix->N, w.qslot, Q, out, st);
+             }), "gather");
+  ET_API_END
+}
+
+et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, const float* luts,
+                        const float* queries, int64_t Q, int32_t k, float* dist, int32_t* ids, void* workspace,
+                        size_t ws, void* stream) {
+  ET_API_BEGIN
+  if (!ix || !dist || !ids) fail(ET_ERR_CONFIG, "null argument");
+  if (ix->kind == kIvf) fail(ET_ERR_CONFIG, "use et_ivf_topk for IVF indexes");
+  if (k < 1 || k > kTopkMax) fail(ET_ERR_CONFIG, "k must be 1..256");
+  if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
+  if (Q == 0) { g_err.clear(); return ET_OK; }
+  ScanParams sp;
+  table_source(sp, ix, codebooks, d, luts, queries);
+  const int nsm = num_sms();
+  Plan pl = make_plan(ix, Q, k, nsm);
+  const size_t need = ws_bytes(ix, pl, Q, false, 1);
+  if (!workspace || ws < need) fail(ET_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  Carve c{reinterpret_cast<char*>(workspace), 0, ws};
+  Work w = carve(c, ix, pl, Q, false, 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  cuda_check(timed("fill", st, [&] { return launch_fill_flat(Q, pl.n_chunks, w.chunk_q, w.qslot_off, w.qslot, st); }), "fill");
+  fill_scan_common(sp, ix, pl);
+  sp.chunk_q = w.chunk_q;
+  sp.lut0 = w.lut0;
+  sp.partials = w.partials;
+  sp.mode = kModeTopk;
+  sp.k = k;
+  sp.B = pl.B;
+  sp.cand = w.cand;
+  sp.cand_cnt = w.cand_cnt;
+  sp.unit_thr = w.unit_thr;
+  cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
+  FinParams fp;
+  fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
+  fp.qslot_off = w.qslot_off; fp.qslot = w.qslot;
+  fp.cand = w.cand; fp.cand_cnt = w.cand_cnt;
+  fp.group_off = ix->group_off.as<uint32_t>();
+  fp.ids = ix->ids.as<int32_t>();
+  fp.group_mult = ix->group_mult.as<uint32_t>();
+  fp.group_minid = ix->group_minid.as<int32_t>();
+  fp.unit_thr = w.unit_thr;
+  fp.out_dist = dist; fp.out_ids = ids;
+  cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
+  ET_API_END
+}
+
+et_status et_ivf_topk(const et_index*, const float*, int64_t, int32_t, int32_t, float*, int32_t*, int32_t*, void*,
+                      size_t, void*) {
+  g_err = "et_ivf_topk: not built yet";
+  return ET_ERR_CONFIG;
+}
+
+et_status et_merge_topk(const float* in_dist, const int32_t* in_ids, int32_t G, int64_t Q, int32_t k,
+                        float* out_dist, int32_t* out_ids, void* stream) {
+  ET_API_BEGIN
+  if (G < 1 || k < 1 || k > kTopkMax) fail(ET_ERR_CONFIG, "bad G or k");
+  if (Q <= 0) { g_err.clear(); return ET_OK; }
+  if (!in_dist || !in_ids || !out_dist || !out_ids) fail(ET_ERR_CONFIG, "null argument");
+  cuda_check(launch_merge(in_dist, in_ids, G, Q, k, out_dist, out_ids, (cudaStream_t)stream), "merge");
+  ET_API_END
+}
+
+et_status et_flat_adc(const float* luts, int64_t Q, int32_t M, int32_t K, const uint8_t* codes, int64_t n,
+                      float* out, void* stream) {
+  ET_API_BEGIN
+  if (M <= 0 || K <= 0 || K > 256) fail(ET_ERR_CONFIG, "bad M/K");
+  if (Q <= 0 || n <= 0) { g_err.clear(); return ET_OK; }
+  if (!luts || !codes || !out) fail(ET_ERR_CONFIG, "null argument");
+  cuda_check(launch_flat_adc(luts, Q, M, K, codes, n, out, (cudaStream_t)stream), "flat_adc");
+  ET_API_END
+}
+
+et_status et_encode(const float* codebooks, int32_t d, int32_t M, int32_t K, const float* x, int64_t n,
+                    const float* centroids, const int32_t* assign, uint8_t* codes, void* stream) {
+  ET_API_BEGIN
+  if (M <= 0 || K <= 0 || K > 256) fail(ET_ERR_CONFIG, "bad M/K");
+  if (d <= 0 || d % M) fail(ET_ERR_SUBSPACE_SPLIT, "d % M != 0");
+  if ((centroids == nullptr) != (assign == nullptr)) fail(ET_ERR_CONFIG, "centroids and assign go together");
+  if (n <= 0) { g_err.clear(); return ET_OK; }
+  if (!codebooks || !x || !codes) fail(ET_ERR_CONFIG, "null argument");
+  if ((size_t)K * (d / M) * 4 > 200 * 1024) fail(ET_ERR_CONFIG, "codebook of one subspace exceeds shared memory");
+  cuda_check(launch_encode(codebooks, d, M, K, x, n, centroids, assign, codes, (cudaStream_t)stream), "encode");
+  ET_API_END
+}
+
+et_status et_assign(const float* centroids, int32_t nlist, int32_t d, const float* x, int64_t n, int32_t* assign,
+                    void* stream) {
+  ET_API_BEGIN
+  if (nlist < 1 || d < 1) fail(ET_ERR_CONFIG, "bad nlist/d");
+  if (n <= 0) { g_err.clear(); return ET_OK; }
+  if (!centroids || !x || !assign) fail(ET_ERR_CONFIG, "null argument");
+  if ((size_t)32 * d * 4 > 200 * 1024) fail(ET_ERR_CONFIG, "d too large");
+  cuda_check(launch_assign(centroids, nlist, d, x, n, assign, nullptr, (cudaStream_t)stream), "assign");
+  ET_API_END
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// k-means (et_build_codebooks): k-means++ on the host (fp64, splitmix64 RNG),
+// Lloyd with the GPU encode kernel as the assignment step, fp64 updates.
+// ---------------------------------------------------------------------------
+namespace et {
+
+static inline uint64_t splitmix64(uint64_t& s) {
+  uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static inline double u01(uint64_t& s) { return (splitmix64(s) >> 11) * (1.0 / 9007199254740992.0); }
+
+static void kmeanspp_sub(const float* train, int64_t n, int d, int off, int s, int K, uint64_t seed,
+                         double* C /* K*s */) {
+  uint64_t rs = seed;
+  std::vector<double> D(n);
+  auto dist = [&](int64_t i, const double* c) {
+    const float* x = train + (size_t)i * d + off;
+    double a = 0;
+    for (int j = 0; j < s; ++j) { const double t = (double)x[j] - c[j]; a += t * t; }
+    return a;
+  };
+  int64_t i0 = (int64_t)(splitmix64(rs) % (uint64_t)n);
+  for (int j = 0; j < s; ++j) C[j] = train[(size_t)i0 * d + off + j];
+  double tot = 0;
+  for (int64_t i = 0; i < n; ++i) { D[i] = dist(i, C); tot += D[i]; }
+  for (int k = 1; k < K; ++k) {
+    int64_t pick;
+    if (tot <= 0) pick = (int64_t)(splitmix64(rs) % (uint64_t)n);
+    else {
+      const double u = u01(rs) * tot;
+      double acc = 0;
+      pick = n - 1;
+      for (int64_t i = 0; i < n; ++i) { acc += D[i]; if (acc > u) { pick = i; break; } }
+    }
+    double* ck = C + (size_t)k * s;
+    for (int j = 0; j < s; ++j) ck[j] = train[(size_t)pick * d + off + j];
+    tot = 0;
+    for (int64_t i = 0; i < n; ++i) { D[i] = std::min(D[i], dist(i, ck)); tot += D[i]; }
+  }
+}
+
+}  // namespace et
+
+extern "C" et_status et_build_codebooks(const float* train, int64_t n, int32_t d, int32_t M, int32_t K,
+                                        int32_t lloyd_iters, uint64_t seed, float* codebooks,
+                                        double* objective_hist) {
+  ET_API_BEGIN
+  if (!train || !codebooks) fail(ET_ERR_CONFIG, "null argument");
+  if (M <= 0 || d <= 0 || d % M) fail(ET_ERR_SUBSPACE_SPLIT, "d % M != 0");
+  if (K <= 0 || K > 256) fail(ET_ERR_CONFIG, "K must be 1..256");
+  if (n < K) fail(ET_ERR_INSUFFICIENT_DATA, "n < K");
+  if (lloyd_iters < 1) fail(ET_ERR_CONFIG, "lloyd_iters >= 1");
+  for (int64_t i = 0; i < n * d; ++i)
+    if (!std::isfinite(train[i])) fail(ET_ERR_INVALID_VECTOR, "non-finite training value");
+  const int s = d / M;
+  std::vector<double> C((size_t)M * K * s);
+  {
+    std::vector<std::thread> th;
+    for (int m = 0; m < M; ++m)
+      th.emplace_back(kmeanspp_sub, train, n, d, m * s, s, K, seed * 1000003ull + (uint64_t)m, C.data() + (size_t)m * K * s);
+    for (auto& t : th) t.join();
+  }
+  float* dx = nullptr; float* dc = nullptr; uint8_t* dcodes = nullptr;
+  auto cleanup = [&]() { if (dx) cudaFree(dx); if (dc) cudaFree(dc); if (dcodes) cudaFree(dcodes); };
+  try {
+    cuda_check(cudaMalloc(&dx, (size_t)n * d * 4), "cudaMalloc(train)");
+    cuda_check(cudaMalloc(&dc, (size_t)M * K * s * 4), "cudaMalloc(cb)");
+    cuda_check(cudaMalloc(&dcodes, (size_t)n * M), "cudaMalloc(codes)");
+    cuda_check(cudaMemcpy(dx, train, (size_t)n * d * 4, cudaMemcpyHostToDevice), "upload train");
+    std::vector<float> Cf((size_t)M * K * s);
+    std::vector<uint8_t> codes((size_t)n * M);
+    for (int it = 0; it < lloyd_iters; ++it) {
+      for (size_t i = 0; i < Cf.size(); ++i) Cf[i] = (float)C[i];
+      cuda_check(cudaMemcpy(dc, Cf.data(), Cf.size() * 4, cudaMemcpyHostToDevice), "upload cb");
+      cuda_check(launch_encode(dc, d, M, K, dx, n, nullptr, nullptr, dcodes, 0), "assign");
+      cuda_check(cudaMemcpy(codes.data(), dcodes, codes.size(), cudaMemcpyDeviceToHost), "download codes");
+      for (int m = 0; m < M; ++m) {
+        std::vector<double> sum((size_t)K * s, 0.0), far(n);
+        std::vector<int64_t> cnt(K, 0);
+        double obj = 0;
+        const float* cm = Cf.data() + (size_t)m * K * s;
+        for (int64_t i = 0; i < n; ++i) {
+          const int k = codes[(size_t)i * M + m];
+          const float* x = train + (size_t)i * d + m * s;
+          double a = 0;
+          for (int j = 0; j < s; ++j) {
+            const double t = (double)x[j] - (double)cm[(size_t)k * s + j];
+            a += t * t;
+            sum[(size_t)k * s + j] += x[j];
+          }
+          far[i] = a;
+          obj += a;
+          ++cnt[k];
+        }
+        if (objective_hist) objective_hist[(size_t)m * lloyd_iters + it] = obj;
+        std::vector<int64_t> order;
+        for (int k = 0; k < K; ++k) {
+          double* ck = C.data() + ((size_t)m * K + k) * s;
+          if (cnt[k] > 0) {
+            for (int j = 0; j < s; ++j) ck[j] = sum[(size_t)k * s + j] / (double)cnt[k];
+          } else {   // empty cluster -> farthest point from its assigned centroid
+            if (order.empty()) {
+              order.resize(n);
+              std::iota(order.begin(), order.end(), 0);
+              std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return far[a] > far[b]; });
+            }
+            int64_t pick = order.front();
+            order.erase(order.begin());
+            for (int j = 0; j < s; ++j) ck[j] = train[(size_t)pick * d + m * s + j];
+          }
+        }
+      }
+    }
+    for (size_t i = 0; i < C.size(); ++i) codebooks[i] = (float)C[i];
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  ET_API_END
+}

@@ -1,0 +1,113 @@
+// internal.h -- structures shared by the host build (host.cpp) and the sm_100a
+// kernels (kernels.cu) of libetree.  Not part of the C ABI (see include/etree.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace et {
+
+constexpr int kWarps = 16;                 // warps per scan CTA (1 CTA / SM: the tables fill smem)
+constexpr int kThreads = kWarps * 32;
+constexpr int kMaxTrees = 4;               // E-Forest trees supported by one index
+constexpr int kMaxMT = 8;                  // levels (code bytes) per tree on the GPU
+constexpr int kKMax = 256;                 // codewords per subspace (one byte)
+constexpr int kTopkMax = 256;              // largest k of the fused top-k
+constexpr int kFinWarps = 8;               // warps per finalize CTA
+
+// One tree of the device layout ("leaf-major HMS"): the leaves in
+// depth-first (= lexicographic) order, each with its full projected code and
+// the length of its common prefix with the previous leaf.  The internal nodes
+// of the paper's Hierarchical Memory Structure are implicit: a leaf whose LCP
+// with its predecessor is p enters the new internal nodes at depths p..depth-1,
+// whose K fields are the leaf's own code bytes.
+struct TreeDev {
+  int MT = 0;                  // levels of this tree
+  int layer0 = 0;              // first code byte it covers
+  int64_t n_leaves = 0;
+  const uint64_t* code = nullptr;   // byte l of the code at bits 8l..8l+7
+  const uint8_t* lcp = nullptr;     // LCP with the previous leaf (0 for leaf 0)
+};
+
+enum ScanMode : int { kModeFull = 0, kModeTopk = 1 };
+
+struct ScanParams {
+  // ---- distance-table source ----
+  const float* codebooks = nullptr;   // [M][K][s]        (fused tables)
+  const float* queries = nullptr;     // [Q][d]           (fused tables)
+  const float* luts = nullptr;        // [Q][M][K]        (materialised tables) or null
+  const float* coarse = nullptr;      // [nlist][d]       (IVF residual tables) or null
+  const int* layer_sub = nullptr;     // [M] subspace of each code byte (chunk order)
+  int d = 0, M = 0, K = 0, s = 0;
+  // ---- work decomposition ----
+  int n_units = 0;                    // CTAs = n_chunks * S
+  int S = 1;                          // leaf segments per chunk
+  const int* chunk_q = nullptr;       // [n_chunks][32] query of each lane, -1 = idle (active lanes first)
+  const int* chunk_cell = nullptr;    // [n_chunks] coarse cell (IVF) or null
+  const uint32_t* chunk_lo = nullptr; // [n_chunks] tree-0 leaf range (IVF lists) or null
+  const uint32_t* chunk_hi = nullptr;
+  // ---- trees / groups ----
+  int T = 1;
+  TreeDev tree[kMaxTrees];
+  const uint32_t* t0_tup_off = nullptr;            // forest: [L2_0+1] tuples of each tree-0 leaf
+  const uint32_t* tup_leaf[kMaxTrees] = {};        // forest: [n_groups] leaf of tuple in tree t>=1
+  const uint32_t* group_mult = nullptr;            // [n_groups] ids per group
+  const int32_t* group_minid = nullptr;            // [n_groups] smallest id of the group
+  int64_t n_groups = 0;
+  // ---- scratch ----
+  float* lut0 = nullptr;              // [n_units][256][32] level-0 tables when MT == 8
+  float* partials = nullptr;          // forest: per unit, trees 1..T-1: [L2_t][32]
+  int64_t part_base[kMaxTrees] = {};  // offset of tree t's block inside a unit's partials
+  int64_t part_stride = 0;            // floats per unit
+  // ---- outputs ----
+  int mode = kModeTopk;
+  float* leafdist = nullptr;          // FULL: [n_chunks][n_groups][32]
+  int k = 0;                          // TOPK
+  int B = 0;                          // candidate buffer capacity per (unit, warp, lane)
+  uint2* cand = nullptr;              // [n_units][kWarps][32][B] (dist bits, group)
+  int* cand_cnt = nullptr;            // [n_units][kWarps][32]
+  float* unit_thr = nullptr;          // [n_units][32] final CTA threshold per lane
+  int vec4 = 1;                       // query/codebook rows 16-byte aligned
+};
+
+struct FinParams {
+  int64_t Q = 0;
+  int k = 0, B = 0, S = 1;
+  const int* qslot_off = nullptr;     // [Q+1]
+  const int* qslot = nullptr;         // chunk*32 + lane for each (query, probe)
+  const uint2* cand = nullptr;
+  const int* cand_cnt = nullptr;
+  const uint32_t* group_off = nullptr;  // [n_groups+1]
+  const int32_t* ids = nullptr;         // [N] grouped, ascending within a group
+  const uint32_t* group_mult = nullptr;
+  const int32_t* group_minid = nullptr;
+  const float* unit_thr = nullptr;      // [n_units][32] or null
+  float* out_dist = nullptr;
+  int32_t* out_ids = nullptr;
+};
+
+// ---- launchers (kernels.cu); each returns cudaGetLastError() ----
+size_t scan_smem_bytes(int MTmax);
+cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st);
+cudaError_t launch_finalize(const FinParams& p, cudaStream_t st);
+cudaError_t launch_fill_flat(int64_t Q, int n_chunks, int* chunk_q, int* qslot_off, int* qslot,
+                             cudaStream_t st);
+cudaError_t launch_gather_full(const float* leafdist, const uint32_t* slot2group,
+                               int64_t n_groups, int64_t n, const int* qslot, int64_t Q,
+                               float* out, cudaStream_t st);
+cudaError_t launch_luts(const float* codebooks, int d, int M, int K, const float* queries,
+                        int64_t Q, float* luts, bool vec4, cudaStream_t st);
+cudaError_t launch_flat_adc(const float* luts, int64_t Q, int M, int K, const uint8_t* codes,
+                            int64_t n, float* out, cudaStream_t st);
+cudaError_t launch_encode(const float* codebooks, int d, int M, int K, const float* x, int64_t n,
+                          const float* centroids, const int32_t* assign, uint8_t* codes,
+                          cudaStream_t st);
+cudaError_t launch_assign(const float* centroids, int nlist, int d, const float* x, int64_t n,
+                          int32_t* assign, float* best_dist, cudaStream_t st);
+cudaError_t launch_probe(const float* centroids, int nlist, int d, const float* queries, int64_t Q,
+                         int w, int32_t* probes, cudaStream_t st);
+cudaError_t launch_merge(const float* in_dist, const int32_t* in_ids, int G, int64_t Q, int k,
+                         float* out_dist, int32_t* out_ids, cudaStream_t st);
+void count_launch(int n = 1);
+
+}  // namespace et

@@ -1,0 +1,1050 @@
+// kernels.cu -- sm_100a kernels of libetree (E-Tree / E-Forest ADC, arXiv 1509.05186).
+//
+// K1  lut_kernel            distance tables, materialised [Q][M][K]
+// K2  scan_kernel           fused tables + Distance-Context scan + emit
+//                           (full output P:244/P:257, or top-k candidates), E-Forest
+//                           join for T >= 2
+// K4  finalize_kernel       exact top-k by (distance, id) with leaf multiplicities
+//     gather_full_kernel    out[q][slot] = leaf distance of slot's leaf (full output)
+// K5  flat_adc_kernel       naive ADC comparison
+// K7  merge_kernel          merge G shard top-k lists
+// K8  encode_kernel         PQ encode argmin, residual variant for IVF
+//     assign_kernel         nearest coarse centroid
+//
+// Design notes are in DESIGN.md §4-5; every floating-point table entry is the
+// direct difference sum_j (x_j - c_j)^2 accumulated in fp32 with j ascending.
+#include "internal.h"
+
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+#include <algorithm>
+
+namespace et {
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
+// ---------------------------------------------------------------------------
+// table build helpers
+// ---------------------------------------------------------------------------
+
+// Swizzled shared-memory table: entry (level, k, lane) of the CTA's 32 queries.
+// A lookup by warp-uniform (level, k) with lane = query touches 32 consecutive
+// words (conflict-free); a build store with lanes = 32 consecutive codewords and
+// a uniform query slot i lands on bank (i ^ lane): also conflict-free.
+__device__ __forceinline__ int tab_index(int lvl, int k, int i) {
+  return ((lvl << 8) + k) * 32 + (i ^ (k & 31));
+}
+
+// Squared distance between the query sub-vector x[0..s) (optionally minus the
+// coarse centroid cc) and codeword c (registers), fp32, j ascending, FMA.
+template <int SS>
+struct Codeword {
+  float c[SS];
+  __device__ __forceinline__ void load(const float* row) {
+#pragma unroll
+    for (int j = 0; j < SS; j += 4) {
+      float4 v = __ldg(reinterpret_cast<const float4*>(row + j));
+      c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
+    }
+  }
+};
+
+// Computes table entries for queries slots [0, nq) and codeword `crow` (one per
+// lane).  `xq(i)` returns the pointer to slot i's sub-vector; `cc` is the coarse
+// centroid sub-vector (IVF) or null.  `store(i, v)` writes the entry.
+template <int SS, class XQ, class ST>
+__device__ __forceinline__ void entries_fixed(const float* crow, bool kvalid, int nq,
+                                              XQ xq, const float* cc, ST store) {
+  Codeword<SS> cw;
+  if (kvalid) cw.load(crow);
+  else {
+#pragma unroll
+    for (int j = 0; j < SS; ++j) cw.c[j] = 0.f;
+  }
+  int i = 0;
+  for (; i + 4 <= nq; i += 4) {
+    const float4* x0 = reinterpret_cast<const float4*>(xq(i));
+    const float4* x1 = reinterpret_cast<const float4*>(xq(i + 1));
+    const float4* x2 = reinterpret_cast<const float4*>(xq(i + 2));
+    const float4* x3 = reinterpret_cast<const float4*>(xq(i + 3));
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int jb = 0; jb < SS / 4; ++jb) {
+      float4 v0 = __ldg(x0 + jb), v1 = __ldg(x1 + jb), v2 = __ldg(x2 + jb), v3 = __ldg(x3 + jb);
+      if (cc) {
+        float4 cv = __ldg(reinterpret_cast<const float4*>(cc) + jb);
+        v0.x -= cv.x; v0.y -= cv.y; v0.z -= cv.z; v0.w -= cv.w;
+        v1.x -= cv.x; v1.y -= cv.y; v1.z -= cv.z; v1.w -= cv.w;
+        v2.x -= cv.x; v2.y -= cv.y; v2.z -= cv.z; v2.w -= cv.w;
+        v3.x -= cv.x; v3.y -= cv.y; v3.z -= cv.z; v3.w -= cv.w;
+      }
+      const float* c = cw.c + 4 * jb;
+      float t;
+      t = v0.x - c[0]; a0 = fmaf(t, t, a0); t = v0.y - c[1]; a0 = fmaf(t, t, a0);
+      t = v0.z - c[2]; a0 = fmaf(t, t, a0); t = v0.w - c[3]; a0 = fmaf(t, t, a0);
+      t = v1.x - c[0]; a1 = fmaf(t, t, a1); t = v1.y - c[1]; a1 = fmaf(t, t, a1);
+      t = v1.z - c[2]; a1 = fmaf(t, t, a1); t = v1.w - c[3]; a1 = fmaf(t, t, a1);
+      t = v2.x - c[0]; a2 = fmaf(t, t, a2); t = v2.y - c[1]; a2 = fmaf(t, t, a2);
+      t = v2.z - c[2]; a2 = fmaf(t, t, a2); t = v2.w - c[3]; a2 = fmaf(t, t, a2);
+      t = v3.x - c[0]; a3 = fmaf(t, t, a3); t = v3.y - c[1]; a3 = fmaf(t, t, a3);
+      t = v3.z - c[2]; a3 = fmaf(t, t, a3); t = v3.w - c[3]; a3 = fmaf(t, t, a3);
+    }
+    store(i, a0); store(i + 1, a1); store(i + 2, a2); store(i + 3, a3);
+  }
+  for (; i < nq; ++i) {
+    const float4* x0 = reinterpret_cast<const float4*>(xq(i));
+    float a0 = 0.f;
+#pragma unroll
+    for (int jb = 0; jb < SS / 4; ++jb) {
+      float4 v0 = __ldg(x0 + jb);
+      if (cc) {
+        float4 cv = __ldg(reinterpret_cast<const float4*>(cc) + jb);
+        v0.x -= cv.x; v0.y -= cv.y; v0.z -= cv.z; v0.w -= cv.w;
+      }
+      const float* c = cw.c + 4 * jb;
+      float t;
+      t = v0.x - c[0]; a0 = fmaf(t, t, a0); t = v0.y - c[1]; a0 = fmaf(t, t, a0);
+      t = v0.z - c[2]; a0 = fmaf(t, t, a0); t = v0.w - c[3]; a0 = fmaf(t, t, a0);
+    }
+    store(i, a0);
+  }
+}
+
+// Generic sub-vector length (any s): scalar loads.
+template <class XQ, class ST>
+__device__ __forceinline__ void entries_generic(const float* crow, bool kvalid, int s, int nq,
+                                                XQ xq, const float* cc, ST store) {
+  for (int i = 0; i < nq; ++i) {
+    const float* x = xq(i);
+    float a = 0.f;
+    for (int j = 0; j < s; ++j) {
+      float xv = __ldg(x + j);
+      if (cc) xv -= __ldg(cc + j);
+      float t = xv - (kvalid ? __ldg(crow + j) : 0.f);
+      a = fmaf(t, t, a);
+    }
+    store(i, a);
+  }
+}
+
+template <int SS, class XQ, class ST>
+__device__ __forceinline__ void entries(const float* crow, bool kvalid, int s, int nq, XQ xq,
+                                        const float* cc, ST store) {
+  if constexpr (SS > 0) entries_fixed<SS>(crow, kvalid, nq, xq, cc, store);
+  else entries_generic(crow, kvalid, s, nq, xq, cc, store);
+}
+
+// ---------------------------------------------------------------------------
+// K2: the scan kernel
+// ---------------------------------------------------------------------------
+
+struct SmemScan {
+  float* tab;          // [(levels)][256][32] swizzled
+  unsigned* thr;       // [32] CTA-shared top-k thresholds (float bits)
+  int* qidx;           // [32] query of each lane
+  int* cnt;            // [kWarps][32] per-warp candidate counts (end of unit)
+};
+
+// Build the tables of tree t for this CTA's queries.  Levels 0..MT-1 of the
+// tree; level 0 goes to the global scratch lut0 when MT == 8 (7 levels fill
+// the 227 KB of shared memory), everything else to shared memory.
+template <int SS>
+__device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq, int cell) {
+  const TreeDev& tr = p.tree[t];
+  const int MT = tr.MT;
+  const int lv0 = (MT == 8) ? 1 : 0;
+  const int K = p.K, s = p.s, d = p.d;
+  const int nb = (K + 31) >> 5;
+  const int lane = lane_id();
+  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
+  for (int item = warp_id(); item < MT * nb; item += kWarps) {
+    const int l = item / nb, kb = item - l * nb;
+    const int k = kb * 32 + lane;
+    const bool kvalid = k < K;
+    const int m = p.layer_sub[tr.layer0 + l];
+    auto store = [&](int i, float v) {
+      if (!kvalid) return;
+      if (l < lv0) lut0[k * 32 + i] = v;
+      else sm.tab[tab_index(l - lv0, k, i)] = v;
+    };
+    if (p.luts) {  // materialised tables: copy
+      for (int i = 0; i < nq; ++i) {
+        float v = kvalid ? __ldg(p.luts + ((size_t)sm.qidx[i] * p.M + m) * K + k) : 0.f;
+        store(i, v);
+      }
+      continue;
+    }
+    const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s;
+    const float* cc = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + (size_t)m * s : nullptr;
+    auto xq = [&](int i) { return p.queries + (size_t)sm.qidx[i] * d + (size_t)m * s; };
+    entries<SS>(crow, kvalid, s, nq, xq, cc, store);
+  }
+}
+
+// Warp-cooperative pruning of one lane's candidate buffer (rare; see DESIGN.md
+// §4.3).  Keeps every candidate that can still be among the query's k smallest
+// (distance, id) pairs: t = smallest distance whose cumulative multiplicity
+// reaches k; all candidates < t; of the candidates == t, those whose smallest
+// id ranks below k - (multiplicity < t).  Returns the new count and threshold.
+constexpr int kRefreshPer = (2 * kTopkMax + 96) / 32;   // entries per lane held in registers
+
+__device__ __noinline__ void refresh_buffer(uint2* buf, int n, int k, const uint32_t* gmult,
+                                            const int32_t* gminid, int* new_cnt, float* new_thr) {
+  const int lane = lane_id();
+  uint32_t key[kRefreshPer], grp[kRefreshPer], mul[kRefreshPer];
+#pragma unroll
+  for (int r = 0; r < kRefreshPer; ++r) {
+    const int i = r * 32 + lane;
+    if (i < n) {
+      uint2 e = buf[i];
+      key[r] = e.x; grp[r] = e.y; mul[r] = __ldg(gmult + e.y);
+    } else {
+      key[r] = 0xffffffffu; grp[r] = 0; mul[r] = 0;
+    }
+  }
+  // total multiplicity
+  uint32_t tot = 0;
+#pragma unroll
+  for (int r = 0; r < kRefreshPer; ++r) tot += mul[r];
+  tot = __reduce_add_sync(FULLMASK, tot);
+  if (tot < (uint32_t)k) {  // cannot prune (only possible with a tiny k vs B; keep all)
+    *new_cnt = n; *new_thr = __int_as_float(0x7f800000); return;
+  }
+  uint32_t v = 0;
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t cand = v | ((1u << bit) - 1u);
+    uint32_t c = 0;
+#pragma unroll
+    for (int r = 0; r < kRefreshPer; ++r) c += (key[r] <= cand) ? mul[r] : 0u;
+    c = __reduce_add_sync(FULLMASK, c);
+    if (c < (uint32_t)k) v |= (1u << bit);
+  }
+  const uint32_t t = v;
+  uint32_t slt = 0, ntied = 0;
+#pragma unroll
+  for (int r = 0; r < kRefreshPer; ++r) {
+    slt += (key[r] < t) ? mul[r] : 0u;
+    ntied += (key[r] == t) ? 1u : 0u;
+  }
+  slt = __reduce_add_sync(FULLMASK, slt);
+  ntied = __reduce_add_sync(FULLMASK, ntied);
+  const uint32_t R = (uint32_t)k - slt;
+  uint32_t tau = 0xffffffffu;
+  uint32_t mid[kRefreshPer];
+#pragma unroll
+  for (int r = 0; r < kRefreshPer; ++r) mid[r] = 0xffffffffu;
+  if (ntied > R) {
+#pragma unroll
+    for (int r = 0; r < kRefreshPer; ++r)
+      if (key[r] == t) mid[r] = (uint32_t)__ldg(gminid + grp[r]);
+    uint32_t w = 0;
+    for (int bit = 31; bit >= 0; --bit) {
+      const uint32_t cand = w | ((1u << bit) - 1u);
+      uint32_t c = 0;
+#pragma unroll
+      for (int r = 0; r < kRefreshPer; ++r) c += (key[r] == t && mid[r] <= cand) ? 1u : 0u;
+      c = __reduce_add_sync(FULLMASK, c);
+      if (c < R) w |= (1u << bit);
+    }
+    tau = w;
+  }
+  __syncwarp();
+  int base = 0;
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < kRefreshPer; ++r) {
+    const bool keep = (r * 32 + lane < n) && (key[r] < t || (key[r] == t && (ntied <= R || mid[r] <= tau)));
+    const unsigned m = __ballot_sync(FULLMASK, keep);
+    if (keep) buf[base + __popc(m & lt)] = make_uint2(key[r], grp[r]);
+    base += __popc(m);
+  }
+  __syncwarp();
+  *new_cnt = base;
+  *new_thr = __uint_as_float(t);
+}
+
+// Per-lane top-k candidate state.
+struct TopkState {
+  float thr;
+  int cnt;
+  uint2* buf;         // this lane's buffer
+  uint2* warp_buf;    // lane 0's buffer (lane L's = warp_buf + L*B)
+  bool active;
+};
+
+struct EmitCtx {
+  const ScanParams* p;
+  int role;           // 0: forest partial (tree t>=1), 1: tree-0 leaves are the groups, 2: forest tuples
+  int t;              // tree index for role 0
+  int unit, chunk;
+  float* part;        // this unit's partials base
+  TopkState ts;
+};
+
+__device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, uint32_t mult) {
+  const ScanParams& p = *e.p;
+  const int lane = lane_id();
+  if (p.mode == kModeFull) {
+    p.leafdist[((size_t)e.chunk * p.n_groups + g) * 32 + lane] = dist;
+    return;
+  }
+  TopkState& ts = e.ts;
+  const bool pass = ts.active && dist <= ts.thr;
+  if (__any_sync(FULLMASK, pass)) {
+    if (pass) {
+      ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), g);
+      ++ts.cnt;
+      if (mult >= (uint32_t)p.k) ts.thr = dist;   // one group alone bounds the k-th distance
+    }
+    unsigned full = __ballot_sync(FULLMASK, ts.cnt >= p.B);
+    while (full) {
+      const int L = __ffs(full) - 1;
+      full &= full - 1;
+      int nc; float nt;
+      const int n = __shfl_sync(FULLMASK, ts.cnt, L);
+      refresh_buffer(ts.warp_buf + (size_t)L * p.B, n, p.k, p.group_mult, p.group_minid, &nc, &nt);
+      if (lane == L) { ts.cnt = nc; ts.thr = fminf(ts.thr, nt); }
+    }
+  }
+}
+
+// Distance-Context update over the levels p..MT-1 of one leaf (P:249 for the
+// internal levels, P:239-243 for the leaf and its postfix): ctx[l] =
+// ctx[l-1] + T[l][code byte l], summed left to right exactly like naive ADC.
+#define ET_LEVEL(L)                                                                     \
+  case L:                                                                               \
+    if constexpr (L < MT) {                                                             \
+      const uint32_t kb = (L < 4) ? ((lo >> (8 * (L & 3))) & 255u) : ((hi >> (8 * (L & 3))) & 255u); \
+      float v;                                                                          \
+      if (L < lv0) v = lut0g[kb * 32 + lane];                                           \
+      else v = tab[tab_index(L - lv0, kb, lane)];                                       \
+      ctx[L] = (L == 0) ? v : ctx[L > 0 ? L - 1 : 0] + v;                               \
+    }                                                                                   \
+    [[fallthrough]];
+
+template <int MT>
+__device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b,
+                          const float* lut0g) {
+  const ScanParams& p = *e.p;
+  constexpr int lv0 = (MT == 8) ? 1 : 0;
+  const int lane = lane_id();
+  const float* tab = sm.tab;
+  float ctx[MT];
+#pragma unroll
+  for (int l = 0; l < MT; ++l) ctx[l] = 0.f;
+  const bool topk = p.mode == kModeTopk;
+  int batch = 0;
+  for (uint32_t base = a; base < b; base += 32, ++batch) {
+    const uint32_t idx = base + lane;
+    const bool in = idx < b;
+    const uint64_t mycode = in ? __ldg(tr.code + idx) : 0ull;
+    const uint32_t mylcp = in ? (uint32_t)__ldg(tr.lcp + idx) : 0u;
+    uint32_t aux0 = 0, aux1 = 0;   // role 1: multiplicity; role 2: tuple range
+    if (e.role == 1 && topk && in) aux0 = __ldg(p.group_mult + idx);
+    if (e.role == 2 && in) { aux0 = __ldg(p.t0_tup_off + idx); aux1 = __ldg(p.t0_tup_off + idx + 1); }
+    const int n = (int)min(32u, b - base);
+    for (int j = 0; j < n; ++j) {
+      const uint32_t lo = __shfl_sync(FULLMASK, (uint32_t)mycode, j);
+      const uint32_t hi = __shfl_sync(FULLMASK, (uint32_t)(mycode >> 32), j);
+      int pl = (int)__shfl_sync(FULLMASK, mylcp, j);
+      if (base + j == a) pl = 0;   // first leaf of this warp's range: rebuild the whole path
+      switch (pl) {
+        ET_LEVEL(0) ET_LEVEL(1) ET_LEVEL(2) ET_LEVEL(3) ET_LEVEL(4) ET_LEVEL(5) ET_LEVEL(6) ET_LEVEL(7)
+        default: break;
+      }
+      const float dist = ctx[MT - 1];
+      const uint32_t leaf = base + j;
+      if (e.role == 0) {
+        e.part[(size_t)p.part_base[e.t] + (size_t)leaf * 32 + lane] = dist;
+      } else if (e.role == 1) {
+        const uint32_t mult = __shfl_sync(FULLMASK, aux0, j);
+        emit_group(e, dist, leaf, mult);
+      } else {
+        const uint32_t t0 = __shfl_sync(FULLMASK, aux0, j);
+        const uint32_t t1 = __shfl_sync(FULLMASK, aux1, j);
+        for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
+          float dd = dist;
+          for (int tt = 1; tt < p.T; ++tt) {
+            const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
+            dd = dd + e.part[(size_t)p.part_base[tt] + (size_t)lf * 32 + lane];
+          }
+          const uint32_t mult = topk ? __ldg(p.group_mult + g) : 0u;
+          emit_group(e, dd, g, mult);
+        }
+      }
+    }
+    if (topk && e.role != 0) {   // share the threshold with the CTA's other warps
+      if (e.ts.active) {
+        atomicMin(&sm.thr[lane], __float_as_uint(e.ts.thr));
+        e.ts.thr = __uint_as_float(*((volatile unsigned*)&sm.thr[lane]));
+      }
+    }
+  }
+}
+#undef ET_LEVEL
+
+__device__ __forceinline__ void scan_dispatch(EmitCtx& e, const SmemScan& sm, const TreeDev& tr,
+                                              uint32_t a, uint32_t b, const float* lut0g) {
+  switch (tr.MT) {
+    case 1: scan_tree<1>(e, sm, tr, a, b, lut0g); break;
+    case 2: scan_tree<2>(e, sm, tr, a, b, lut0g); break;
+    case 3: scan_tree<3>(e, sm, tr, a, b, lut0g); break;
+    case 4: scan_tree<4>(e, sm, tr, a, b, lut0g); break;
+    case 5: scan_tree<5>(e, sm, tr, a, b, lut0g); break;
+    case 6: scan_tree<6>(e, sm, tr, a, b, lut0g); break;
+    case 7: scan_tree<7>(e, sm, tr, a, b, lut0g); break;
+    case 8: scan_tree<8>(e, sm, tr, a, b, lut0g); break;
+    default: break;
+  }
+}
+
+template <int SS>
+__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int unit = blockIdx.x;
+  const int chunk = unit / p.S;
+  const int seg = unit - chunk * p.S;
+  const int lane = lane_id(), warp = warp_id();
+  int MTmax = 0;
+  for (int t = 0; t < p.T; ++t) MTmax = max(MTmax, p.tree[t].MT);
+  const int smem_levels = (MTmax == 8) ? 7 : MTmax;
+  SmemScan sm;
+  sm.tab = reinterpret_cast<float*>(smem_raw);
+  sm.thr = reinterpret_cast<unsigned*>(smem_raw + (size_t)smem_levels * 256 * 32 * 4);
+  sm.qidx = reinterpret_cast<int*>(sm.thr + 32);
+  sm.cnt = sm.qidx + 32;
+
+  if (threadIdx.x < 32) {
+    sm.qidx[lane] = __ldg(p.chunk_q + (size_t)chunk * 32 + lane);
+    sm.thr[lane] = 0x7f800000u;   // +inf
+  }
+  __syncthreads();
+  int nq = 0;
+  {
+    const int q = sm.qidx[lane];
+    nq = __popc(__ballot_sync(FULLMASK, q >= 0));   // active lanes are a prefix
+  }
+  const int cell = p.chunk_cell ? __ldg(p.chunk_cell + chunk) : -1;
+  const float* lut0g = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
+
+  EmitCtx e;
+  e.p = &p;
+  e.unit = unit;
+  e.chunk = chunk;
+  e.part = p.partials ? p.partials + (size_t)unit * p.part_stride : nullptr;
+  e.ts.active = lane < nq;
+  e.ts.thr = e.ts.active ? __int_as_float(0x7f800000) : -1.0f;
+  e.ts.cnt = 0;
+  e.ts.warp_buf = nullptr;
+  e.ts.buf = nullptr;
+  if (p.mode == kModeTopk) {
+    e.ts.warp_buf = p.cand + ((size_t)(unit * kWarps + warp) * 32) * p.B;
+    e.ts.buf = e.ts.warp_buf + (size_t)lane * p.B;
+  }
+
+  // Forest: trees T-1..1 first (per-leaf partials for this CTA's queries),
+  // then tree 0, whose leaves walk their tuples and sum in tree order.
+  for (int t = p.T - 1; t >= 0; --t) {
+    const TreeDev& tr = p.tree[t];
+    build_tables<SS>(p, sm, t, unit, nq, cell);
+    __syncthreads();
+    uint32_t lo = 0, hi = (uint32_t)tr.n_leaves;
+    if (t == 0) {
+      if (p.chunk_lo) { lo = __ldg(p.chunk_lo + chunk); hi = __ldg(p.chunk_hi + chunk); }
+      const uint32_t len = hi - lo;
+      const uint32_t a = lo + (uint32_t)(((uint64_t)len * seg) / p.S);
+      const uint32_t b = lo + (uint32_t)(((uint64_t)len * (seg + 1)) / p.S);
+      lo = a; hi = b;
+    }
+    const uint32_t len = hi - lo;
+    const uint32_t wa = lo + (uint32_t)(((uint64_t)len * warp) / kWarps);
+    const uint32_t wb = lo + (uint32_t)(((uint64_t)len * (warp + 1)) / kWarps);
+    e.t = t;
+    e.role = (t > 0) ? 0 : (p.T == 1 ? 1 : 2);
+    if (wa < wb) scan_dispatch(e, sm, tr, wa, wb, lut0g);
+    __syncthreads();   // partials visible / tables free for the next tree
+  }
+
+  if (p.mode == kModeTopk) {
+    p.cand_cnt[(size_t)(unit * kWarps + warp) * 32 + lane] = e.ts.cnt;
+    if (warp == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + lane] = __uint_as_float(sm.thr[lane]);
+  }
+}
+
+size_t scan_smem_bytes(int MTmax) {
+  const int levels = (MTmax == 8) ? 7 : MTmax;
+  return (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + kWarps * 32 * 4;
+}
+
+template <int SS>
+static cudaError_t launch_scan_t(const ScanParams& p, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  scan_kernel<SS><<<p.n_units, kThreads, smem, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st) {
+  if (p.n_units <= 0) return cudaSuccess;
+  const size_t smem = scan_smem_bytes(MTmax);
+  const bool v4 = (p.luts == nullptr) && (p.d % 4 == 0) && p.vec4;
+  switch (v4 ? p.s : 0) {
+    case 4: return launch_scan_t<4>(p, smem, st);
+    case 8: return launch_scan_t<8>(p, smem, st);
+    case 16: return launch_scan_t<16>(p, smem, st);
+    case 32: return launch_scan_t<32>(p, smem, st);
+    case 60: return launch_scan_t<60>(p, smem, st);
+    default: return launch_scan_t<0>(p, smem, st);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// warp bitonic sort of n (power of two, <= 512) u64 keys in shared memory
+// ---------------------------------------------------------------------------
+__device__ void warp_bitonic_sort(unsigned long long* a, int n) {
+  const int lane = lane_id();
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncwarp();
+      for (int i = lane; i < n / 2; i += 32) {
+        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        unsigned long long x = a[lo], y = a[hi];
+        if ((x > y) == up) { a[lo] = y; a[hi] = x; }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// K4: finalize -- exact top-k per query over the candidates of all its units
+// ---------------------------------------------------------------------------
+constexpr int kFinCap = 768;   // candidates staged in shared memory per warp
+
+struct FinSmem {
+  uint32_t key[kFinWarps][kFinCap];
+  uint32_t grp[kFinWarps][kFinCap];
+  uint32_t hist[kFinWarps][256];
+  unsigned long long stage[kFinWarps][kTopkMax];
+  int nstage[kFinWarps];
+};
+
+// Enumerates the candidates of query q: smem copy when they fit, else global.
+struct CandSrc {
+  const FinParams* p;
+  int s0, s1;
+  bool in_smem;
+  int n;               // staged count (smem)
+  const uint32_t* key;
+  const uint32_t* grp;
+  float thr;           // prefilter: candidates above every unit's final threshold are dead
+  template <class F>
+  __device__ void each(F f) const {
+    const int lane = lane_id();
+    if (in_smem) {
+      for (int i = lane; i < n; i += 32) f(key[i], grp[i]);
+      return;
+    }
+    const uint32_t tb = __float_as_uint(thr);
+    for (int j = s0; j < s1; ++j) {
+      const int slot = __ldg(p->qslot + j);
+      const int chunk = slot >> 5, ln = slot & 31;
+      for (int sg = 0; sg < p->S; ++sg) {
+        const int unit = chunk * p->S + sg;
+        for (int w = 0; w < kWarps; ++w) {
+          const size_t sb = (size_t)(unit * kWarps + w) * 32 + ln;
+          const int c = __ldg(p->cand_cnt + sb);
+          const uint2* eb = p->cand + sb * p->B;
+          for (int i = lane; i < c; i += 32) {
+            const uint2 v = eb[i];
+            if (v.x <= tb) f(v.x, v.y);
+          }
+        }
+      }
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParams p) {
+  const float* unit_thr = p.unit_thr;
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  FinSmem& fs = *reinterpret_cast<FinSmem*>(fsm_raw);
+  const int lane = lane_id(), warp = warp_id();
+  const int64_t q = (int64_t)blockIdx.x * kFinWarps + warp;
+  if (q >= p.Q) return;
+  const int k = p.k;
+  const int s0 = p.qslot_off[q], s1 = p.qslot_off[q + 1];
+
+  // 1. threshold prefilter: min over the query's units of their final thresholds
+  float thr = __int_as_float(0x7f800000);
+  if (unit_thr) {
+    for (int j = s0; j < s1; ++j) {
+      const int slot = __ldg(p.qslot + j);
+      const int chunk = slot >> 5, ln = slot & 31;
+      for (int sg = lane; sg < p.S; sg += 32)
+        thr = fminf(thr, __ldg(unit_thr + (size_t)(chunk * p.S + sg) * 32 + ln));
+    }
+    for (int o = 16; o > 0; o >>= 1) thr = fminf(thr, __shfl_xor_sync(FULLMASK, thr, o));
+  }
+  const uint32_t tb = __float_as_uint(thr);
+
+  // 2. stage candidates (<= thr) into shared memory
+  int n = 0;
+  bool overflow = false;
+  {
+    uint32_t* K_ = fs.key[warp];
+    uint32_t* G_ = fs.grp[warp];
+    for (int j = s0; j < s1 && !overflow; ++j) {
+      const int slot = __ldg(p.qslot + j);
+      const int chunk = slot >> 5, ln = slot & 31;
+      for (int sg = 0; sg < p.S && !overflow; ++sg) {
+        const int unit = chunk * p.S + sg;
+        // counts of the 16 warps of this unit: one load per lane
+        const int myc = (lane < kWarps) ? __ldg(p.cand_cnt + (size_t)(unit * kWarps + lane) * 32 + ln) : 0;
+        for (int w = 0; w < kWarps; ++w) {
+          const int c = __shfl_sync(FULLMASK, myc, w);
+          if (c == 0) continue;
+          const uint2* eb = p.cand + ((size_t)(unit * kWarps + w) * 32 + ln) * p.B;
+          for (int i0 = 0; i0 < c; i0 += 32) {
+            const int i = i0 + lane;
+            uint2 v = make_uint2(0xffffffffu, 0);
+            if (i < c) v = eb[i];
+            const bool keep = (i < c) && v.x <= tb;
+            const unsigned m = __ballot_sync(FULLMASK, keep);
+            const int pos = n + __popc(m & ((1u << lane) - 1u));
+            if (keep && pos < kFinCap) { K_[pos] = v.x; G_[pos] = v.y; }
+            n += __popc(m);
+          }
+          if (n > kFinCap) { overflow = true; break; }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  CandSrc src;
+  src.p = &p; src.s0 = s0; src.s1 = s1; src.in_smem = !overflow; src.n = n;
+  src.key = fs.key[warp]; src.grp = fs.grp[warp]; src.thr = thr;
+
+  // 3. weighted radix select: t = smallest distance with cumulative multiplicity >= k
+  uint32_t* hist = fs.hist[warp];
+  uint32_t prefix = 0, pmask = 0, need = (uint32_t)k;
+  bool all = false;
+  uint32_t total = 0;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int i = lane; i < 256; i += 32) hist[i] = 0;
+    __syncwarp();
+    src.each([&](uint32_t key, uint32_t g) {
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], __ldg(p.group_mult + g));
+    });
+    __syncwarp();
+    uint32_t h[8], loc = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) { h[r] = hist[lane * 8 + r]; loc += h[r]; }
+    uint32_t inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULLMASK, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const uint32_t tot = __shfl_sync(FULLMASK, inc, 31);
+    if (pass == 0) total = tot;
+    if (tot < need) { all = true; break; }   // fewer than k ids in total
+    const uint32_t excl = inc - loc;
+    // the lane whose bins contain the crossing
+    const bool mine = excl < need && need <= inc;
+    const unsigned who = __ballot_sync(FULLMASK, mine);
+    const int L = __ffs(who) - 1;
+    uint32_t digit = 0, before = 0;
+    if (lane == L) {
+      uint32_t c = excl;
+      for (int r = 0; r < 8; ++r) {
+        if (c + h[r] >= need) { digit = lane * 8 + r; before = c; break; }
+        c += h[r];
+      }
+    }
+    digit = __shfl_sync(FULLMASK, digit, L);
+    before = __shfl_sync(FULLMASK, before, L);
+    need -= before;
+    prefix |= digit << shift;
+    pmask |= 255u << shift;
+  }
+  const uint32_t t = all ? 0xffffffffu : prefix;
+
+  // 4. collect ids: all of every group < t, then the R smallest ids among tied groups
+  unsigned long long* stage = fs.stage[warp];
+  if (lane == 0) fs.nstage[warp] = 0;
+  __syncwarp();
+  uint32_t slt = 0, ntied = 0;
+  src.each([&](uint32_t key, uint32_t g) {
+    if (key < t || all) {
+      const uint32_t o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
+      slt += o1 - o0;
+      const int pos = atomicAdd(&fs.nstage[warp], (int)(o1 - o0));
+      for (uint32_t o = o0; o < o1; ++o)
+        if (pos + (int)(o - o0) < kTopkMax)
+          stage[pos + (o - o0)] = ((unsigned long long)key << 32) | (uint32_t)__ldg(p.ids + o);
+    } else if (key == t) {
+      ntied += 1;
+    }
+  });
+  slt = __reduce_add_sync(FULLMASK, slt);
+  ntied = __reduce_add_sync(FULLMASK, ntied);
+  if (!all && ntied > 0) {
+    const uint32_t R = (uint32_t)k - slt;
+    // tau: R-th smallest minid among tied groups (only groups with minid <= tau matter)
+    uint32_t tau = 0xffffffffu;
+    if (ntied > R) {
+      uint32_t w = 0;
+      for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t cand = w | ((1u << bit) - 1u);
+        uint32_t c = 0;
+        src.each([&](uint32_t key, uint32_t g) {
+          if (key == t && (uint32_t)__ldg(p.group_minid + g) <= cand) ++c;
+        });
+        c = __reduce_add_sync(FULLMASK, c);
+        if (c < R) w |= (1u << bit);
+      }
+      tau = w;
+    }
+    // sigma: R-th smallest id of the union of those groups' ids
+    auto count_le = [&](uint32_t v) {
+      uint32_t c = 0;
+      src.each([&](uint32_t key, uint32_t g) {
+        if (key != t || (uint32_t)__ldg(p.group_minid + g) > tau) return;
+        uint32_t lo = __ldg(p.group_off + g), hi = __ldg(p.group_off + g + 1);
+        const uint32_t o0 = lo;
+        while (lo < hi) {   // ids ascending within a group
+          const uint32_t mid = (lo + hi) >> 1;
+          if ((uint32_t)__ldg(p.ids + mid) <= v) lo = mid + 1; else hi = mid;
+        }
+        c += lo - o0;
+      });
+      return __reduce_add_sync(FULLMASK, c);
+    };
+    uint32_t sigma = 0xffffffffu;
+    if (count_le(0xfffffffeu) > R) {
+      uint32_t w = 0;
+      for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t cand = w | ((1u << bit) - 1u);
+        if (count_le(cand) < R) w |= (1u << bit);
+      }
+      sigma = w;
+    }
+    src.each([&](uint32_t key, uint32_t g) {
+      if (key != t || (uint32_t)__ldg(p.group_minid + g) > tau) return;
+      const uint32_t o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
+      for (uint32_t o = o0; o < o1; ++o) {
+        const uint32_t id = (uint32_t)__ldg(p.ids + o);
+        if (id > sigma) break;
+        const int pos = atomicAdd(&fs.nstage[warp], 1);
+        if (pos < kTopkMax) stage[pos] = ((unsigned long long)key << 32) | id;
+      }
+    });
+  }
+  __syncwarp();
+  int ns = min(fs.nstage[warp], kTopkMax);
+  int np2 = 32;
+  while (np2 < ns) np2 <<= 1;
+  for (int i = ns + lane; i < np2; i += 32) stage[i] = ~0ull;
+  __syncwarp();
+  warp_bitonic_sort(stage, np2);
+  for (int i = lane; i < k; i += 32) {
+    float dv = __int_as_float(0x7f800000);
+    int32_t iv = -1;
+    if (i < ns) {
+      const unsigned long long v = stage[i];
+      dv = __uint_as_float((uint32_t)(v >> 32));
+      iv = (int32_t)(uint32_t)(v & 0xffffffffu);
+    }
+    p.out_dist[(size_t)q * k + i] = dv;
+    p.out_ids[(size_t)q * k + i] = iv;
+  }
+}
+
+cudaError_t launch_finalize(const FinParams& p, cudaStream_t st) {
+  if (p.Q <= 0) return cudaSuccess;
+  const size_t smem = sizeof(FinSmem);
+  cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)((p.Q + kFinWarps - 1) / kFinWarps);
+  finalize_kernel<<<grid, kFinWarps * 32, smem, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// full output gather: out[q][slot] = leafdist[chunk(q)][group(slot)][lane(q)]
+// ---------------------------------------------------------------------------
+__global__ void gather_full_kernel(const float* __restrict__ leafdist, const uint32_t* __restrict__ slot2group,
+                                   int64_t n_groups, int64_t n, const int* __restrict__ qslot,
+                                   float* __restrict__ out, int use_smem) {
+  extern __shared__ float col[];
+  const int64_t q = blockIdx.y;
+  const int slot = qslot[q];
+  const int chunk = slot >> 5, ln = slot & 31;
+  const float* src = leafdist + (size_t)chunk * n_groups * 32 + ln;
+  if (use_smem) {
+    for (int64_t g = threadIdx.x; g < n_groups; g += blockDim.x) col[g] = __ldg(src + g * 32);
+    __syncthreads();
+  }
+  float* o = out + (size_t)q * n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t g = __ldg(slot2group + i);
+    o[i] = use_smem ? col[g] : __ldg(src + (size_t)g * 32);
+  }
+}
+
+cudaError_t launch_gather_full(const float* leafdist, const uint32_t* slot2group, int64_t n_groups, int64_t n,
+                               const int* qslot, int64_t Q, float* out, cudaStream_t st) {
+  if (Q <= 0 || n <= 0) return cudaSuccess;
+  const size_t smem = (size_t)n_groups * 4;
+  const int use_smem = smem <= 96 * 1024;
+  if (use_smem) {
+    cudaError_t e = cudaFuncSetAttribute(gather_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int bx = (int)std::min<int64_t>((n + 1023) / 1024, 64);
+  for (int64_t q0 = 0; q0 < Q; q0 += 65535) {
+    dim3 grid(bx, (unsigned)std::min<int64_t>(65535, Q - q0));
+    gather_full_kernel<<<grid, 1024, use_smem ? smem : 0, st>>>(leafdist, slot2group, n_groups, n, qslot + q0,
+                                                                 out + (size_t)q0 * n, use_smem);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K1: materialised distance tables [Q][M][K]
+// ---------------------------------------------------------------------------
+template <int SS>
+__global__ void __launch_bounds__(256) lut_kernel(const float* __restrict__ codebooks, int d, int M, int K,
+                                                  const float* __restrict__ queries, int64_t Q,
+                                                  float* __restrict__ luts) {
+  const int m = blockIdx.y;
+  const int s = d / M;
+  const int64_t q0 = (int64_t)blockIdx.x * 32;
+  const int nq = (int)(Q - q0 < 32 ? Q - q0 : 32);
+  for (int k = threadIdx.x; k < ((K + 31) & ~31); k += blockDim.x) {
+    const bool kvalid = k < K;
+    const float* crow = codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s;
+    auto xq = [&](int i) { return queries + (size_t)(q0 + i) * d + (size_t)m * s; };
+    auto store = [&](int i, float v) { if (kvalid) luts[((size_t)(q0 + i) * M + m) * K + k] = v; };
+    entries<SS>(crow, kvalid, s, nq, xq, nullptr, store);
+  }
+}
+
+cudaError_t launch_luts(const float* codebooks, int d, int M, int K, const float* queries, int64_t Q,
+                        float* luts, bool vec4, cudaStream_t st) {
+  if (Q <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((Q + 31) / 32), (unsigned)M);
+  const int s = d / M;
+  switch ((vec4 && d % 4 == 0) ? s : 0) {
+    case 4: lut_kernel<4><<<grid, 256, 0, st>>>(codebooks, d, M, K, queries, Q, luts); break;
+    case 8: lut_kernel<8><<<grid, 256, 0, st>>>(codebooks, d, M, K, queries, Q, luts); break;
+    case 16: lut_kernel<16><<<grid, 256, 0, st>>>(codebooks, d, M, K, queries, Q, luts); break;
+    case 32: lut_kernel<32><<<grid, 256, 0, st>>>(codebooks, d, M, K, queries, Q, luts); break;
+    case 60: lut_kernel<60><<<grid, 256, 0, st>>>(codebooks, d, M, K, queries, Q, luts); break;
+    default: lut_kernel<0><<<grid, 256, 0, st>>>(codebooks, d, M, K, queries, Q, luts); break;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K5: naive ADC (comparison): out[q][i] = sum_m T[q][m][code_i[m]], m ascending
+// ---------------------------------------------------------------------------
+__global__ void flat_adc_kernel(const float* __restrict__ luts, int64_t Q, int M, int K,
+                                const uint8_t* __restrict__ codes, int64_t n, float* __restrict__ out) {
+  const int64_t q = blockIdx.y;
+  const float* T = luts + (size_t)q * M * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t* c = codes + (size_t)i * M;
+    float acc = __ldg(T + c[0]);
+    for (int m = 1; m < M; ++m) acc = acc + __ldg(T + (size_t)m * K + c[m]);
+    out[(size_t)q * n + i] = acc;
+  }
+}
+
+cudaError_t launch_flat_adc(const float* luts, int64_t Q, int M, int K, const uint8_t* codes, int64_t n,
+                            float* out, cudaStream_t st) {
+  if (Q <= 0 || n <= 0) return cudaSuccess;
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)Q);
+  flat_adc_kernel<<<grid, 256, 0, st>>>(luts, Q, M, K, codes, n, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K8: encode (argmin per subspace, ties -> lowest k), optional residual
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) encode_kernel(const float* __restrict__ codebooks, int d, int M, int K,
+                                                     const float* __restrict__ x, int64_t n,
+                                                     const float* __restrict__ centroids,
+                                                     const int32_t* __restrict__ assign, uint8_t* __restrict__ codes) {
+  extern __shared__ float cb[];   // [K][s] of subspace m
+  const int m = blockIdx.y;
+  const int s = d / M;
+  for (int i = threadIdx.x; i < K * s; i += blockDim.x) cb[i] = __ldg(codebooks + (size_t)m * K * s + i);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float xs[128];
+  const float* xr = x + (size_t)i * d + (size_t)m * s;
+  const float* cr = centroids ? centroids + (size_t)assign[i] * d + (size_t)m * s : nullptr;
+  float best = __int_as_float(0x7f800000);
+  int bk = 0;
+  if (s <= 128) {
+    for (int j = 0; j < s; ++j) xs[j] = cr ? (__ldg(xr + j) - __ldg(cr + j)) : __ldg(xr + j);
+    for (int k = 0; k < K; ++k) {
+      const float* c = cb + k * s;
+      float a = 0.f;
+      for (int j = 0; j < s; ++j) { const float t = xs[j] - c[j]; a = fmaf(t, t, a); }
+      if (a < best) { best = a; bk = k; }
+    }
+  } else {
+    for (int k = 0; k < K; ++k) {
+      const float* c = cb + k * s;
+      float a = 0.f;
+      for (int j = 0; j < s; ++j) {
+        const float xv = cr ? (__ldg(xr + j) - __ldg(cr + j)) : __ldg(xr + j);
+        const float t = xv - c[j];
+        a = fmaf(t, t, a);
+      }
+      if (a < best) { best = a; bk = k; }
+    }
+  }
+  codes[(size_t)i * M + m] = (uint8_t)bk;
+}
+
+cudaError_t launch_encode(const float* codebooks, int d, int M, int K, const float* x, int64_t n,
+                          const float* centroids, const int32_t* assign, uint8_t* codes, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int s = d / M;
+  const size_t smem = (size_t)K * s * 4;
+  cudaError_t e = cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)M);
+  encode_kernel<<<grid, 256, smem, st>>>(codebooks, d, M, K, x, n, centroids, assign, codes);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// nearest centroid (ties -> lower index); centroids staged through smem in tiles
+__global__ void __launch_bounds__(256) assign_kernel(const float* __restrict__ C, int nlist, int d,
+                                                     const float* __restrict__ x, int64_t n,
+                                                     int32_t* __restrict__ assign, float* __restrict__ best_dist) {
+  extern __shared__ float tile[];  // [TC][d]
+  const int TC = 32;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const float* xr = x + (size_t)(i < n ? i : n - 1) * d;
+  float best = __int_as_float(0x7f800000);
+  int bi = 0;
+  for (int c0 = 0; c0 < nlist; c0 += TC) {
+    const int nc = min(TC, nlist - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * d; e += blockDim.x) tile[e] = __ldg(C + (size_t)c0 * d + e);
+    __syncthreads();
+    for (int c = 0; c < nc; ++c) {
+      const float* cr = tile + c * d;
+      float a = 0.f;
+      for (int j = 0; j < d; ++j) { const float t = __ldg(xr + j) - cr[j]; a = fmaf(t, t, a); }
+      if (a < best) { best = a; bi = c0 + c; }
+    }
+  }
+  if (i < n) {
+    assign[i] = bi;
+    if (best_dist) best_dist[i] = best;
+  }
+}
+
+cudaError_t launch_assign(const float* centroids, int nlist, int d, const float* x, int64_t n,
+                          int32_t* assign, float* best_dist, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = (size_t)32 * d * 4;
+  cudaError_t e = cudaFuncSetAttribute(assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  assign_kernel<<<(unsigned)((n + 255) / 256), 256, smem, st>>>(centroids, nlist, d, x, n, assign, best_dist);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K7: merge G shard lists per query (warp per query)
+// ---------------------------------------------------------------------------
+__global__ void merge_kernel(const float* __restrict__ in_dist, const int32_t* __restrict__ in_ids, int G,
+                             int64_t Q, int k, float* __restrict__ out_dist, int32_t* __restrict__ out_ids) {
+  __shared__ unsigned long long buf[4][2 * kTopkMax];
+  const int lane = lane_id(), warp = warp_id();
+  const int64_t q = (int64_t)blockIdx.x * 4 + warp;
+  if (q >= Q) return;
+  unsigned long long* a = buf[warp];
+  int np2 = 32;
+  while (np2 < k) np2 <<= 1;
+  auto load = [&](int g, unsigned long long* dst) {
+    for (int i = lane; i < np2; i += 32) {
+      unsigned long long v = ~0ull;
+      if (i < k) {
+        const size_t o = ((size_t)g * Q + q) * k + i;
+        const int32_t id = in_ids[o];
+        if (id >= 0) v = ((unsigned long long)__float_as_uint(in_dist[o]) << 32) | (uint32_t)id;
+      }
+      dst[i] = v;
+    }
+  };
+  load(0, a);
+  __syncwarp();
+  warp_bitonic_sort(a, np2);
+  for (int g = 1; g < G; ++g) {
+    load(g, a + np2);
+    __syncwarp();
+    warp_bitonic_sort(a, 2 * np2);
+  }
+  for (int i = lane; i < k; i += 32) {
+    const unsigned long long v = a[i];
+    out_dist[(size_t)q * k + i] = (v == ~0ull) ? __int_as_float(0x7f800000) : __uint_as_float((uint32_t)(v >> 32));
+    out_ids[(size_t)q * k + i] = (v == ~0ull) ? -1 : (int32_t)(uint32_t)(v & 0xffffffffu);
+  }
+}
+
+cudaError_t launch_merge(const float* in_dist, const int32_t* in_ids, int G, int64_t Q, int k,
+                         float* out_dist, int32_t* out_ids, cudaStream_t st) {
+  if (Q <= 0) return cudaSuccess;
+  merge_kernel<<<(unsigned)((Q + 3) / 4), 128, 0, st>>>(in_dist, in_ids, G, Q, k, out_dist, out_ids);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// chunk_q / qslot for the flat plan: chunk c holds queries [c*Q/n, (c+1)*Q/n)
+__global__ void fill_flat_kernel(int64_t Q, int n_chunks, int* chunk_q, int* qslot_off, int* qslot) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < (int64_t)n_chunks * 32) {
+    const int c = (int)(t >> 5), i = (int)(t & 31);
+    const int64_t s = (int64_t)c * Q / n_chunks, e = (int64_t)(c + 1) * Q / n_chunks;
+    const bool act = s + i < e;
+    chunk_q[t] = act ? (int)(s + i) : -1;
+    if (act) qslot[s + i] = c * 32 + i;
+  }
+  if (t <= Q) qslot_off[t] = (int)t;
+}
+
+cudaError_t launch_fill_flat(int64_t Q, int n_chunks, int* chunk_q, int* qslot_off, int* qslot, cudaStream_t st) {
+  const int64_t n = std::max<int64_t>((int64_t)n_chunks * 32, Q + 1);
+  fill_flat_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Q, n_chunks, chunk_q, qslot_off, qslot);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe(const float*, int, int, const float*, int64_t, int, int32_t*, cudaStream_t) {
+  return cudaErrorNotSupported;  // IVF probe: see ivf.cu
+}
+
+}  // namespace et
