@@ -143,7 +143,7 @@ struct et_index {
   et::DevBuf group_off, ids, group_mult, group_minid, slot2group;
   et::DevBuf t0_tup_off, tup_leaf[et::kMaxTrees];
   et::DevBuf layer_sub_d;
-  et::DevBuf coarse, codebooks;      // IVF
+  et::DevBuf coarse, coarse_t, codebooks;   // IVF ([nlist][d], [d][nlist], [M][K][s])
   std::vector<uint32_t> list_leaf_off;
   et::DevBuf list_leaf_off_d;
   double lookups_per_query = 0;      // sum over trees (+ tuples) -- planning
@@ -498,6 +498,12 @@ static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t 
   ix->stats[0] = tot;
   ix->list_leaf_off_d.upload(ix->list_leaf_off);
   ix->coarse.upload_raw(coarse, (size_t)nlist * d * 4);
+  {
+    std::vector<float> ct((size_t)nlist * d);
+    for (int c = 0; c < nlist; ++c)
+      for (int j = 0; j < d; ++j) ct[(size_t)j * nlist + c] = coarse[(size_t)c * d + j];
+    ix->coarse_t.upload(ct);
+  }
   ix->codebooks.upload_raw(codebooks, (size_t)M * K * (d / M) * 4);
   ix->lookups_per_query = (double)tot.lookups / std::max(1, nlist);
   return ix.release();
@@ -560,6 +566,19 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   return pl;
 }
 
+// IVF: chunks are (cell, <= 32 probing queries); their number is data
+// dependent, bounded by ceil(Q*w/32) + nlist (one partial chunk per cell).
+static Plan make_ivf_plan(const et_index* ix, int64_t Q, int w, int k) {
+  Plan pl;
+  pl.MTmax = ix->M;
+  pl.lut0 = (pl.MTmax == 8);
+  pl.n_chunks = (int)((Q * w + 31) / 32 + ix->nlist);
+  pl.S = 1;
+  pl.n_units = pl.n_chunks;
+  pl.B = topk_B(std::max(1, k));
+  return pl;
+}
+
 struct Carve {
   char* base;
   size_t off = 0, cap;
@@ -598,6 +617,31 @@ static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool 
 static size_t ws_bytes(const et_index* ix, const Plan& pl, int64_t Q, bool full, int slots_per_q) {
   Carve c{nullptr, 0, 0};
   carve(c, ix, pl, Q, full, slots_per_q);
+  return c.off + 256;
+}
+
+struct IvfWork {
+  int32_t* probes; int* cell_cnt; int* pair_pos; int* chunk_off; int* n_chunks;
+  int* chunk_cell; uint32_t* chunk_lo; uint32_t* chunk_hi;
+};
+
+static IvfWork carve_ivf(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, int w) {
+  IvfWork v{};
+  v.probes = c.take<int32_t>((size_t)Q * w);
+  v.cell_cnt = c.take<int>(ix->nlist);
+  v.pair_pos = c.take<int>((size_t)Q * w);
+  v.chunk_off = c.take<int>(ix->nlist + 1);
+  v.n_chunks = c.take<int>(1);
+  v.chunk_cell = c.take<int>(pl.n_chunks);
+  v.chunk_lo = c.take<uint32_t>(pl.n_chunks);
+  v.chunk_hi = c.take<uint32_t>(pl.n_chunks);
+  return v;
+}
+
+static size_t ivf_ws_bytes(const et_index* ix, const Plan& pl, int64_t Q, int w) {
+  Carve c{nullptr, 0, 0};
+  carve_ivf(c, ix, pl, Q, w);
+  carve(c, ix, pl, Q, false, w);
   return c.off + 256;
 }
 
@@ -777,7 +821,13 @@ et_status et_workspace_size(const et_index* ix, int64_t Q, int32_t k, int32_t np
   if (!ix || !bytes) fail(ET_ERR_CONFIG, "null argument");
   if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
   const int nsm = num_sms();
-  if (ix->kind == kIvf) fail(ET_ERR_CONFIG, "IVF workspace: use et_ivf_workspace_size");
+  if (ix->kind == kIvf) {
+    if (nprobe < 1 || nprobe > ix->nlist) fail(ET_ERR_CONFIG, "nprobe must be 1..nlist");
+    Plan pl = make_ivf_plan(ix, std::max<int64_t>(Q, 1), nprobe, k);
+    *bytes = ivf_ws_bytes(ix, pl, std::max<int64_t>(Q, 1), nprobe);
+    g_err.clear();
+    return ET_OK;
+  }
   const bool full = (k <= 0);
   Plan pl = make_plan(ix, std::max<int64_t>(Q, 1), full ? 1 : k, nsm);
   *bytes = ws_bytes(ix, pl, std::max<int64_t>(Q, 1), full, 1);
@@ -862,10 +912,65 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   ET_API_END
 }
 
-et_status et_ivf_topk(const et_index*, const float*, int64_t, int32_t, int32_t, float*, int32_t*, int32_t*, void*,
-                      size_t, void*) {
-  g_err = "et_ivf_topk: not built yet";
-  return ET_ERR_CONFIG;
+et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32_t nprobe, int32_t k,
+                      float* dist, int32_t* ids, int32_t* probes, void* workspace, size_t ws, void* stream) {
+  ET_API_BEGIN
+  if (!ix || !queries || !dist || !ids) fail(ET_ERR_CONFIG, "null argument");
+  if (ix->kind != kIvf) fail(ET_ERR_CONFIG, "not an IVF index");
+  if (k < 1 || k > kTopkMax) fail(ET_ERR_CONFIG, "k must be 1..256");
+  if (nprobe < 1 || nprobe > ix->nlist) fail(ET_ERR_CONFIG, "nprobe must be 1..nlist");
+  if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
+  if (Q == 0) { g_err.clear(); return ET_OK; }
+  if ((size_t)Q * nprobe >= (size_t)INT32_MAX / 2) fail(ET_ERR_CONFIG, "Q * nprobe too large");
+  Plan pl = make_ivf_plan(ix, Q, nprobe, k);
+  const size_t need = ivf_ws_bytes(ix, pl, Q, nprobe);
+  if (!workspace || ws < need) fail(ET_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  Carve c{reinterpret_cast<char*>(workspace), 0, ws};
+  IvfWork v = carve_ivf(c, ix, pl, Q, nprobe);
+  Work w = carve(c, ix, pl, Q, false, nprobe);
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* pr = probes ? probes : v.probes;
+  cuda_check(timed("probe", st, [&] {
+               return launch_probe(ix->coarse_t.as<float>(), ix->nlist, ix->d, queries, Q, nprobe, pr, st);
+             }), "probe");
+  cuda_check(timed("bucket", st, [&] {
+               return launch_ivf_bucket(pr, Q, nprobe, ix->nlist, ix->list_leaf_off_d.as<uint32_t>(), v.cell_cnt,
+                                        v.pair_pos, v.chunk_off, v.n_chunks, v.chunk_cell, v.chunk_lo, v.chunk_hi,
+                                        w.chunk_q, pl.n_chunks, w.qslot_off, w.qslot, st);
+             }), "bucket");
+  ScanParams sp;
+  sp.queries = queries;
+  sp.codebooks = ix->codebooks.as<float>();
+  sp.coarse = ix->coarse.as<float>();
+  sp.d = ix->d;
+  sp.s = ix->d / ix->M;
+  sp.vec4 = aligned16(queries) && (ix->d % 4 == 0) ? 1 : 0;
+  fill_scan_common(sp, ix, pl);
+  sp.chunk_q = w.chunk_q;
+  sp.chunk_cell = v.chunk_cell;
+  sp.chunk_lo = v.chunk_lo;
+  sp.chunk_hi = v.chunk_hi;
+  sp.n_chunks_dev = v.n_chunks;
+  sp.lut0 = w.lut0;
+  sp.mode = kModeTopk;
+  sp.k = k;
+  sp.B = pl.B;
+  sp.cand = w.cand;
+  sp.cand_cnt = w.cand_cnt;
+  sp.unit_thr = w.unit_thr;
+  cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(ivf)");
+  FinParams fp;
+  fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
+  fp.qslot_off = w.qslot_off; fp.qslot = w.qslot;
+  fp.cand = w.cand; fp.cand_cnt = w.cand_cnt;
+  fp.group_off = ix->group_off.as<uint32_t>();
+  fp.ids = ix->ids.as<int32_t>();
+  fp.group_mult = ix->group_mult.as<uint32_t>();
+  fp.group_minid = ix->group_minid.as<int32_t>();
+  fp.unit_thr = w.unit_thr;
+  fp.out_dist = dist; fp.out_ids = ids;
+  cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
+  ET_API_END
 }
 
 et_status et_merge_topk(const float* in_dist, const int32_t* in_ids, int32_t G, int64_t Q, int32_t k,

@@ -46,6 +46,7 @@ struct ScanParams {
   const int* chunk_cell = nullptr;    // [n_chunks] coarse cell (IVF) or null
   const uint32_t* chunk_lo = nullptr; // [n_chunks] tree-0 leaf range (IVF lists) or null
   const uint32_t* chunk_hi = nullptr;
+  const int* n_chunks_dev = nullptr;  // IVF: actual chunk count (device), units beyond it exit
   // ---- trees / groups ----
   int T = 1;
   TreeDev tree[kMaxTrees];
@@ -104,8 +105,12 @@ cudaError_t launch_encode(const float* codebooks, int d, int M, int K, const flo
                           cudaStream_t st);
 cudaError_t launch_assign(const float* centroids, int nlist, int d, const float* x, int64_t n,
                           int32_t* assign, float* best_dist, cudaStream_t st);
-cudaError_t launch_probe(const float* centroids, int nlist, int d, const float* queries, int64_t Q,
+cudaError_t launch_probe(const float* centroids_t, int nlist, int d, const float* queries, int64_t Q,
                          int w, int32_t* probes, cudaStream_t st);
+cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist, const uint32_t* list_leaf_off,
+                              int* cell_cnt, int* pair_pos, int* chunk_off, int* n_chunks, int* chunk_cell,
+                              uint32_t* chunk_lo, uint32_t* chunk_hi, int* chunk_q, int max_chunks,
+                              int* qslot_off, int* qslot, cudaStream_t st);
 cudaError_t launch_merge(const float* in_dist, const int32_t* in_ids, int G, int64_t Q, int k,
                          float* out_dist, int32_t* out_ids, cudaStream_t st);
 void count_launch(int n = 1);

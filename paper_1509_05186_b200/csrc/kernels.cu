@@ -146,42 +146,144 @@ struct SmemScan {
   float* tab;          // [(levels)][256][32] swizzled
   unsigned* thr;       // [32] CTA-shared top-k thresholds (float bits)
   int* qidx;           // [32] query of each lane
-  int* cnt;            // [kWarps][32] per-warp candidate counts (end of unit)
+  float* stage;        // [32 queries][kDC dims] query sub-vector chunk (table build)
 };
 
-// Build the tables of tree t for this CTA's queries.  Levels 0..MT-1 of the
-// tree; level 0 goes to the global scratch lut0 when MT == 8 (7 levels fill
-// the 227 KB of shared memory), everything else to shared memory.
+constexpr int kDC = 16;   // query dimensions staged per table-build pass
+
+// Table entry (level l, codeword k, query slot i): level 0 of an 8-level tree
+// lives in the global scratch row lut0 (7 levels fill shared memory).
+__device__ __forceinline__ float* tab_slot(const SmemScan& sm, float* lut0, int l, int lv0, int k, int i) {
+  return (l < lv0) ? lut0 + k * 32 + i : sm.tab + tab_index(l - lv0, k, i);
+}
+
+// Inner loop of one build pass: codeword chunk c[0..NJ) (registers) against
+// query slots i = g, g+G, ... read from the staged chunk (broadcast loads).
+template <int NJ>
+__device__ __forceinline__ void build_pass_fixed(const SmemScan& sm, float* lut0, int l, int lv0, int k,
+                                                 bool kvalid, const float* crow, int nq, int g, int G,
+                                                 bool first) {
+  float c[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) c[j] = kvalid ? __ldg(crow + j) : 0.f;
+  int i = g;
+  for (; i + G < nq; i += 2 * G) {   // two independent FMA chains
+    const float* x0 = sm.stage + i * kDC;
+    const float* x1 = sm.stage + (i + G) * kDC;
+    float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
+    float* o1 = tab_slot(sm, lut0, l, lv0, k, i + G);
+    float a0 = 0.f, a1 = 0.f;
+    if (!first && kvalid) { a0 = *o0; a1 = *o1; }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const float t0 = x0[j] - c[j];
+      const float t1 = x1[j] - c[j];
+      a0 = fmaf(t0, t0, a0);
+      a1 = fmaf(t1, t1, a1);
+    }
+    if (kvalid) { *o0 = a0; *o1 = a1; }
+  }
+  if (i < nq) {
+    const float* x0 = sm.stage + i * kDC;
+    float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
+    float a0 = (!first && kvalid) ? *o0 : 0.f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const float t0 = x0[j] - c[j];
+      a0 = fmaf(t0, t0, a0);
+    }
+    if (kvalid) *o0 = a0;
+  }
+}
+
+__device__ __forceinline__ void build_pass_generic(const SmemScan& sm, float* lut0, int l, int lv0, int k,
+                                                   bool kvalid, const float* crow, int nj, int nq, int g, int G,
+                                                   bool first) {
+  for (int i = g; i < nq; i += G) {
+    const float* x0 = sm.stage + i * kDC;
+    float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
+    float a0 = (!first && kvalid) ? *o0 : 0.f;
+    for (int j = 0; j < nj; ++j) {
+      const float t0 = x0[j] - (kvalid ? __ldg(crow + j) : 0.f);
+      a0 = fmaf(t0, t0, a0);
+    }
+    if (kvalid) *o0 = a0;
+  }
+}
+
+// Build the tables of tree t for this CTA's queries (fused).
+// Passes over (level, 16-dimension chunk): the chunk of the active queries'
+// sub-vectors (minus the coarse centroid for IVF residuals) is staged in shared
+// memory -- the next pass's values are prefetched into registers while the
+// current pass computes -- and each warp computes 32 codewords (one per lane,
+// codeword chunk in registers) against a share of the queries.  Entries are
+// accumulated across chunks in place, so every entry is the j-ascending fp32
+// FMA chain sum_j (x_j - c_j)^2 regardless of the chunking.
 template <int SS>
 __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq, int cell) {
   const TreeDev& tr = p.tree[t];
   const int MT = tr.MT;
   const int lv0 = (MT == 8) ? 1 : 0;
-  const int K = p.K, s = p.s, d = p.d;
+  const int K = p.K, d = p.d;
+  const int s = (SS > 0) ? SS : p.s;
   const int nb = (K + 31) >> 5;
-  const int lane = lane_id();
+  const int lane = lane_id(), warp = warp_id();
   float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
-  for (int item = warp_id(); item < MT * nb; item += kWarps) {
-    const int l = item / nb, kb = item - l * nb;
-    const int k = kb * 32 + lane;
-    const bool kvalid = k < K;
-    const int m = p.layer_sub[tr.layer0 + l];
-    auto store = [&](int i, float v) {
-      if (!kvalid) return;
-      if (l < lv0) lut0[k * 32 + i] = v;
-      else sm.tab[tab_index(l - lv0, k, i)] = v;
-    };
-    if (p.luts) {  // materialised tables: copy
+  if (p.luts) {   // materialised tables: copy
+    for (int item = warp; item < MT * nb; item += kWarps) {
+      const int l = item / nb, kb = item - l * nb;
+      const int k = kb * 32 + lane;
+      const int m = p.layer_sub[tr.layer0 + l];
       for (int i = 0; i < nq; ++i) {
-        float v = kvalid ? __ldg(p.luts + ((size_t)sm.qidx[i] * p.M + m) * K + k) : 0.f;
-        store(i, v);
+        const float v = (k < K) ? __ldg(p.luts + ((size_t)sm.qidx[i] * p.M + m) * K + k) : 0.f;
+        if (k < K) *tab_slot(sm, lut0, l, lv0, k, i) = v;
       }
-      continue;
     }
-    const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s;
-    const float* cc = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + (size_t)m * s : nullptr;
-    auto xq = [&](int i) { return p.queries + (size_t)sm.qidx[i] * d + (size_t)m * s; };
-    entries<SS>(crow, kvalid, s, nq, xq, cc, store);
+    return;
+  }
+  const int npl = (s + kDC - 1) / kDC;          // passes per level
+  const int P = MT * npl;
+  const int G = max(1, kWarps / nb);            // query groups
+  const int kb = warp % nb, g = warp / nb;
+  const bool computes = g < G;
+  // staging element of this thread: query slot si, dimension sj of the chunk
+  const int si = threadIdx.x / kDC, sj = threadIdx.x % kDC;
+  const int sq = (si < nq) ? sm.qidx[si] : -1;
+  auto fetch = [&](int pass) -> float {
+    const int l = pass / npl, jc = pass - l * npl;
+    const int j = jc * kDC + sj;
+    if (sq < 0 || j >= s) return 0.f;
+    const int m = p.layer_sub[tr.layer0 + l];
+    float v = __ldg(p.queries + (size_t)sq * d + (size_t)m * s + j);
+    if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * s + j);
+    return v;
+  };
+  float nxt = fetch(0);
+  __syncthreads();                              // previous users of the stage are done
+  if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
+  __syncthreads();
+  for (int pass = 0; pass < P; ++pass) {
+    if (pass + 1 < P) nxt = fetch(pass + 1);
+    const int l = pass / npl, jc = pass - l * npl;
+    const int j0 = jc * kDC;
+    const int nj = min(kDC, s - j0);
+    if (computes) {
+      const int k = kb * 32 + lane;
+      const bool kvalid = k < K;
+      const int m = p.layer_sub[tr.layer0 + l];
+      const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s + j0;
+      if constexpr (SS > 0 && SS % kDC == 0) {
+        build_pass_fixed<kDC>(sm, lut0, l, lv0, k, kvalid, crow, nq, g, G, jc == 0);
+      } else if constexpr (SS > 0) {
+        if (nj == kDC) build_pass_fixed<kDC>(sm, lut0, l, lv0, k, kvalid, crow, nq, g, G, jc == 0);
+        else build_pass_fixed<(SS % kDC) ? (SS % kDC) : kDC>(sm, lut0, l, lv0, k, kvalid, crow, nq, g, G, jc == 0);
+      } else {
+        build_pass_generic(sm, lut0, l, lv0, k, kvalid, crow, nj, nq, g, G, jc == 0);
+      }
+    }
+    __syncthreads();
+    if (pass + 1 < P && threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
+    __syncthreads();
   }
 }
 
@@ -315,17 +417,7 @@ __device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, u
 // Distance-Context update over the levels p..MT-1 of one leaf (P:249 for the
 // internal levels, P:239-243 for the leaf and its postfix): ctx[l] =
 // ctx[l-1] + T[l][code byte l], summed left to right exactly like naive ADC.
-#define ET_LEVEL(L)                                                                     \
-  case L:                                                                               \
-    if constexpr (L < MT) {                                                             \
-      const uint32_t kb = (L < 4) ? ((lo >> (8 * (L & 3))) & 255u) : ((hi >> (8 * (L & 3))) & 255u); \
-      float v;                                                                          \
-      if (L < lv0) v = lut0g[kb * 32 + lane];                                           \
-      else v = tab[tab_index(L - lv0, kb, lane)];                                       \
-      ctx[L] = (L == 0) ? v : ctx[L > 0 ? L - 1 : 0] + v;                               \
-    }                                                                                   \
-    [[fallthrough]];
-
+// All lookups of the leaf are issued before the (dependent) additions.
 template <int MT>
 __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b,
                           const float* lut0g) {
@@ -352,10 +444,17 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
       const uint32_t hi = __shfl_sync(FULLMASK, (uint32_t)(mycode >> 32), j);
       int pl = (int)__shfl_sync(FULLMASK, mylcp, j);
       if (base + j == a) pl = 0;   // first leaf of this warp's range: rebuild the whole path
-      switch (pl) {
-        ET_LEVEL(0) ET_LEVEL(1) ET_LEVEL(2) ET_LEVEL(3) ET_LEVEL(4) ET_LEVEL(5) ET_LEVEL(6) ET_LEVEL(7)
-        default: break;
+      float v[MT];
+#pragma unroll
+      for (int l = 0; l < MT; ++l) {
+        if (l >= pl) {
+          const uint32_t kb = ((l < 4 ? lo : hi) >> (8 * (l & 3))) & 255u;
+          v[l] = (l < lv0) ? lut0g[kb * 32 + lane] : tab[tab_index(l - lv0, kb, lane)];
+        }
       }
+#pragma unroll
+      for (int l = 0; l < MT; ++l)
+        if (l >= pl) ctx[l] = (l == 0) ? v[0] : ctx[l > 0 ? l - 1 : 0] + v[l];
       const float dist = ctx[MT - 1];
       const uint32_t leaf = base + j;
       if (e.role == 0) {
@@ -385,7 +484,6 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
     }
   }
 }
-#undef ET_LEVEL
 
 __device__ __forceinline__ void scan_dispatch(EmitCtx& e, const SmemScan& sm, const TreeDev& tr,
                                               uint32_t a, uint32_t b, const float* lut0g) {
@@ -409,6 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanParams p) {
   const int chunk = unit / p.S;
   const int seg = unit - chunk * p.S;
   const int lane = lane_id(), warp = warp_id();
+  if (p.n_chunks_dev && chunk >= *p.n_chunks_dev) return;   // IVF: fewer chunks than the bound
   int MTmax = 0;
   for (int t = 0; t < p.T; ++t) MTmax = max(MTmax, p.tree[t].MT);
   const int smem_levels = (MTmax == 8) ? 7 : MTmax;
@@ -416,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanParams p) {
   sm.tab = reinterpret_cast<float*>(smem_raw);
   sm.thr = reinterpret_cast<unsigned*>(smem_raw + (size_t)smem_levels * 256 * 32 * 4);
   sm.qidx = reinterpret_cast<int*>(sm.thr + 32);
-  sm.cnt = sm.qidx + 32;
+  sm.stage = reinterpret_cast<float*>(sm.qidx + 32);
 
   if (threadIdx.x < 32) {
     sm.qidx[lane] = __ldg(p.chunk_q + (size_t)chunk * 32 + lane);
@@ -477,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanParams p) {
 
 size_t scan_smem_bytes(int MTmax) {
   const int levels = (MTmax == 8) ? 7 : MTmax;
-  return (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + kWarps * 32 * 4;
+  return (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + 32 * kDC * 4;
 }
 
 template <int SS>
@@ -526,17 +625,20 @@ __device__ void warp_bitonic_sort(unsigned long long* a, int n) {
 // ---------------------------------------------------------------------------
 // K4: finalize -- exact top-k per query over the candidates of all its units
 // ---------------------------------------------------------------------------
-constexpr int kFinCap = 768;   // candidates staged in shared memory per warp
+constexpr int kFinCap = 256;   // candidates staged in shared memory per warp
 
 struct FinSmem {
   uint32_t key[kFinWarps][kFinCap];
   uint32_t grp[kFinWarps][kFinCap];
+  uint32_t mul[kFinWarps][kFinCap];
   uint32_t hist[kFinWarps][256];
   unsigned long long stage[kFinWarps][kTopkMax];
   int nstage[kFinWarps];
+  uint32_t tied_g[kFinWarps];
 };
 
 // Enumerates the candidates of query q: smem copy when they fit, else global.
+// f(key, group, multiplicity) is called once per candidate by the owning lane.
 struct CandSrc {
   const FinParams* p;
   int s0, s1;
@@ -544,12 +646,13 @@ struct CandSrc {
   int n;               // staged count (smem)
   const uint32_t* key;
   const uint32_t* grp;
+  const uint32_t* mul;
   float thr;           // prefilter: candidates above every unit's final threshold are dead
   template <class F>
   __device__ void each(F f) const {
     const int lane = lane_id();
     if (in_smem) {
-      for (int i = lane; i < n; i += 32) f(key[i], grp[i]);
+      for (int i = lane; i < n; i += 32) f(key[i], grp[i], mul[i]);
       return;
     }
     const uint32_t tb = __float_as_uint(thr);
@@ -564,7 +667,7 @@ struct CandSrc {
           const uint2* eb = p->cand + sb * p->B;
           for (int i = lane; i < c; i += 32) {
             const uint2 v = eb[i];
-            if (v.x <= tb) f(v.x, v.y);
+            if (v.x <= tb) f(v.x, v.y, __ldg(p->group_mult + v.y));
           }
         }
       }
@@ -573,9 +676,9 @@ struct CandSrc {
 };
 
 __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParams p) {
-  const float* unit_thr = p.unit_thr;
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   FinSmem& fs = *reinterpret_cast<FinSmem*>(fsm_raw);
+  const float* unit_thr = p.unit_thr;
   const int lane = lane_id(), warp = warp_id();
   const int64_t q = (int64_t)blockIdx.x * kFinWarps + warp;
   if (q >= p.Q) return;
@@ -595,54 +698,65 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParam
   }
   const uint32_t tb = __float_as_uint(thr);
 
-  // 2. stage candidates (<= thr) into shared memory
+  // 2. stage candidates (<= thr) into shared memory, with their multiplicities
   int n = 0;
   bool overflow = false;
   {
     uint32_t* K_ = fs.key[warp];
     uint32_t* G_ = fs.grp[warp];
+    uint32_t* U_ = fs.mul[warp];
     for (int j = s0; j < s1 && !overflow; ++j) {
       const int slot = __ldg(p.qslot + j);
       const int chunk = slot >> 5, ln = slot & 31;
       for (int sg = 0; sg < p.S && !overflow; ++sg) {
         const int unit = chunk * p.S + sg;
-        // counts of the 16 warps of this unit: one load per lane
+        // counts of the 16 warps of this unit (one load per lane), prefix sums,
+        // then all lanes load candidates in parallel across the 16 buffers
         const int myc = (lane < kWarps) ? __ldg(p.cand_cnt + (size_t)(unit * kWarps + lane) * 32 + ln) : 0;
-        for (int w = 0; w < kWarps; ++w) {
-          const int c = __shfl_sync(FULLMASK, myc, w);
-          if (c == 0) continue;
-          const uint2* eb = p.cand + ((size_t)(unit * kWarps + w) * 32 + ln) * p.B;
-          for (int i0 = 0; i0 < c; i0 += 32) {
-            const int i = i0 + lane;
-            uint2 v = make_uint2(0xffffffffu, 0);
-            if (i < c) v = eb[i];
-            const bool keep = (i < c) && v.x <= tb;
-            const unsigned m = __ballot_sync(FULLMASK, keep);
-            const int pos = n + __popc(m & ((1u << lane) - 1u));
-            if (keep && pos < kFinCap) { K_[pos] = v.x; G_[pos] = v.y; }
-            n += __popc(m);
-          }
-          if (n > kFinCap) { overflow = true; break; }
+        int inc = myc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULLMASK, inc, o);
+          if (lane >= o) inc += y;
         }
+        const int total = __shfl_sync(FULLMASK, inc, 31);
+        const int excl = inc - myc;
+        for (int i0 = 0; i0 < total; i0 += 32) {
+          const int idx = i0 + lane;
+          int w = 0;
+#pragma unroll
+          for (int st = 8; st >= 1; st >>= 1) {
+            const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
+            if (w + st < kWarps && o <= idx) w += st;
+          }
+          const int wo = __shfl_sync(FULLMASK, excl, w & 31);
+          uint2 v = make_uint2(0xffffffffu, 0);
+          if (idx < total) v = p.cand[((size_t)(unit * kWarps + w) * 32 + ln) * p.B + (idx - wo)];
+          const bool keep = (idx < total) && v.x <= tb;
+          const unsigned m = __ballot_sync(FULLMASK, keep);
+          const int pos = n + __popc(m & ((1u << lane) - 1u));
+          if (keep && pos < kFinCap) { K_[pos] = v.x; G_[pos] = v.y; U_[pos] = __ldg(p.group_mult + v.y); }
+          n += __popc(m);
+        }
+        if (n > kFinCap) overflow = true;
       }
     }
   }
   __syncwarp();
   CandSrc src;
   src.p = &p; src.s0 = s0; src.s1 = s1; src.in_smem = !overflow; src.n = n;
-  src.key = fs.key[warp]; src.grp = fs.grp[warp]; src.thr = thr;
+  src.key = fs.key[warp]; src.grp = fs.grp[warp]; src.mul = fs.mul[warp]; src.thr = thr;
 
   // 3. weighted radix select: t = smallest distance with cumulative multiplicity >= k
   uint32_t* hist = fs.hist[warp];
   uint32_t prefix = 0, pmask = 0, need = (uint32_t)k;
   bool all = false;
-  uint32_t total = 0;
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 24 - 8 * pass;
     for (int i = lane; i < 256; i += 32) hist[i] = 0;
     __syncwarp();
-    src.each([&](uint32_t key, uint32_t g) {
-      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], __ldg(p.group_mult + g));
+    src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], mu);
     });
     __syncwarp();
     uint32_t h[8], loc = 0;
@@ -655,10 +769,8 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParam
       if (lane >= o) inc += y;
     }
     const uint32_t tot = __shfl_sync(FULLMASK, inc, 31);
-    if (pass == 0) total = tot;
-    if (tot < need) { all = true; break; }   // fewer than k ids in total
+    if (tot < need) { all = true; break; }   // fewer than k ids in total (only possible in pass 0)
     const uint32_t excl = inc - loc;
-    // the lane whose bins contain the crossing
     const bool mine = excl < need && need <= inc;
     const unsigned who = __ballot_sync(FULLMASK, mine);
     const int L = __ffs(who) - 1;
@@ -683,21 +795,35 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParam
   if (lane == 0) fs.nstage[warp] = 0;
   __syncwarp();
   uint32_t slt = 0, ntied = 0;
-  src.each([&](uint32_t key, uint32_t g) {
+  src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
     if (key < t || all) {
-      const uint32_t o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
-      slt += o1 - o0;
-      const int pos = atomicAdd(&fs.nstage[warp], (int)(o1 - o0));
-      for (uint32_t o = o0; o < o1; ++o)
-        if (pos + (int)(o - o0) < kTopkMax)
-          stage[pos + (o - o0)] = ((unsigned long long)key << 32) | (uint32_t)__ldg(p.ids + o);
+      const uint32_t o0 = __ldg(p.group_off + g);
+      slt += mu;
+      const int pos = atomicAdd(&fs.nstage[warp], (int)mu);
+      for (uint32_t o = 0; o < mu; ++o)
+        if (pos + (int)o < kTopkMax)
+          stage[pos + o] = ((unsigned long long)key << 32) | (uint32_t)__ldg(p.ids + o0 + o);
     } else if (key == t) {
       ntied += 1;
+      fs.tied_g[warp] = g;
     }
   });
   slt = __reduce_add_sync(FULLMASK, slt);
   ntied = __reduce_add_sync(FULLMASK, ntied);
-  if (!all && ntied > 0) {
+  __syncwarp();
+  if (!all && ntied == 1) {
+    // common case: one group holds the k-th distance -> its R smallest ids
+    const uint32_t R = (uint32_t)k - slt;
+    const uint32_t g = fs.tied_g[warp];
+    const uint32_t o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
+    const uint32_t take = min(R, o1 - o0);
+    const int base = fs.nstage[warp];
+    for (uint32_t i = lane; i < take; i += 32)
+      if (base + (int)i < kTopkMax)
+        stage[base + i] = ((unsigned long long)t << 32) | (uint32_t)__ldg(p.ids + o0 + i);
+    __syncwarp();
+    if (lane == 0) fs.nstage[warp] = base + (int)take;
+  } else if (!all && ntied > 1) {
     const uint32_t R = (uint32_t)k - slt;
     // tau: R-th smallest minid among tied groups (only groups with minid <= tau matter)
     uint32_t tau = 0xffffffffu;
@@ -706,7 +832,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParam
       for (int bit = 31; bit >= 0; --bit) {
         const uint32_t cand = w | ((1u << bit) - 1u);
         uint32_t c = 0;
-        src.each([&](uint32_t key, uint32_t g) {
+        src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
           if (key == t && (uint32_t)__ldg(p.group_minid + g) <= cand) ++c;
         });
         c = __reduce_add_sync(FULLMASK, c);
@@ -717,9 +843,9 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParam
     // sigma: R-th smallest id of the union of those groups' ids
     auto count_le = [&](uint32_t v) {
       uint32_t c = 0;
-      src.each([&](uint32_t key, uint32_t g) {
+      src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
         if (key != t || (uint32_t)__ldg(p.group_minid + g) > tau) return;
-        uint32_t lo = __ldg(p.group_off + g), hi = __ldg(p.group_off + g + 1);
+        uint32_t lo = __ldg(p.group_off + g), hi = lo + mu;
         const uint32_t o0 = lo;
         while (lo < hi) {   // ids ascending within a group
           const uint32_t mid = (lo + hi) >> 1;
@@ -738,11 +864,11 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParam
       }
       sigma = w;
     }
-    src.each([&](uint32_t key, uint32_t g) {
+    src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
       if (key != t || (uint32_t)__ldg(p.group_minid + g) > tau) return;
-      const uint32_t o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
-      for (uint32_t o = o0; o < o1; ++o) {
-        const uint32_t id = (uint32_t)__ldg(p.ids + o);
+      const uint32_t o0 = __ldg(p.group_off + g);
+      for (uint32_t o = 0; o < mu; ++o) {
+        const uint32_t id = (uint32_t)__ldg(p.ids + o0 + o);
         if (id > sigma) break;
         const int pos = atomicAdd(&fs.nstage[warp], 1);
         if (pos < kTopkMax) stage[pos] = ((unsigned long long)key << 32) | id;
@@ -1043,8 +1169,158 @@ cudaError_t launch_fill_flat(int64_t Q, int n_chunks, int* chunk_q, int* qslot_o
   return cudaGetLastError();
 }
 
-cudaError_t launch_probe(const float*, int, int, const float*, int64_t, int, int32_t*, cudaStream_t) {
-  return cudaErrorNotSupported;  // IVF probe: see ivf.cu
+// ---------------------------------------------------------------------------
+// K6: IVF probe -- coarse distances (fp32 direct difference) and the w nearest
+// cells per query by (distance, cell) (Table 1 "w")
+// ---------------------------------------------------------------------------
+template <int QB>
+__global__ void __launch_bounds__(256) probe_kernel(const float* __restrict__ cT, int nlist, int d,
+                                                    const float* __restrict__ queries, int64_t Q, int w,
+                                                    int32_t* __restrict__ probes) {
+  extern __shared__ float psm[];
+  float* qv = psm;                 // [QB][d]
+  float* ds = psm + QB * d;        // [QB][nlist]
+  const int64_t q0 = (int64_t)blockIdx.x * QB;
+  const int nq = (int)((Q - q0) < QB ? (Q - q0) : QB);
+  for (int i = threadIdx.x; i < QB * d; i += blockDim.x) {
+    const int qq = i / d;
+    qv[i] = qq < nq ? __ldg(queries + (size_t)(q0 + qq) * d + (i - qq * d)) : 0.f;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < nlist; c += blockDim.x) {
+    float acc[QB];
+#pragma unroll
+    for (int qq = 0; qq < QB; ++qq) acc[qq] = 0.f;
+#pragma unroll 4
+    for (int j = 0; j < d; ++j) {
+      const float cv = __ldg(cT + (size_t)j * nlist + c);
+#pragma unroll
+      for (int qq = 0; qq < QB; ++qq) {
+        const float t = qv[qq * d + j] - cv;
+        acc[qq] = fmaf(t, t, acc[qq]);
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < QB; ++qq) ds[qq * nlist + c] = acc[qq];
+  }
+  __syncthreads();
+  const int lane = lane_id(), warp = warp_id();
+  for (int qq = warp; qq < nq; qq += blockDim.x / 32) {
+    float* row = ds + qq * nlist;
+    for (int r = 0; r < w; ++r) {
+      float bd = __int_as_float(0x7f800000);
+      int bc = INT_MAX;
+      for (int c = lane; c < nlist; c += 32) {
+        const float v = row[c];
+        if (v < bd || (v == bd && c < bc)) { bd = v; bc = c; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const float od = __shfl_xor_sync(FULLMASK, bd, o);
+        const int oc = __shfl_xor_sync(FULLMASK, bc, o);
+        if (od < bd || (od == bd && oc < bc)) { bd = od; bc = oc; }
+      }
+      if (lane == 0) {
+        probes[(size_t)(q0 + qq) * w + r] = bc;
+        row[bc] = __int_as_float(0x7fc00000);   // NaN: never selected again
+      }
+      __syncwarp();
+    }
+  }
+}
+
+cudaError_t launch_probe(const float* cT, int nlist, int d, const float* queries, int64_t Q, int w,
+                         int32_t* probes, cudaStream_t st) {
+  if (Q <= 0) return cudaSuccess;
+  const size_t budget = 200 * 1024;
+  int qb = 8;
+  while (qb > 1 && (size_t)qb * (nlist + d) * 4 > budget) qb >>= 1;
+  const size_t smem = (size_t)qb * (nlist + d) * 4;
+  if (smem > budget) return cudaErrorInvalidValue;
+  const unsigned grid = (unsigned)((Q + qb - 1) / qb);
+  cudaError_t e;
+#define ET_PROBE(QB_)                                                                               \
+  case QB_:                                                                                         \
+    e = cudaFuncSetAttribute(probe_kernel<QB_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                 \
+    probe_kernel<QB_><<<grid, 256, smem, st>>>(cT, nlist, d, queries, Q, w, probes);                \
+    break;
+  switch (qb) { ET_PROBE(8) ET_PROBE(4) ET_PROBE(2) ET_PROBE(1) default: return cudaErrorInvalidValue; }
+#undef ET_PROBE
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// IVF pair bucketing: (query, probe) pairs grouped by cell into chunks of 32
+// lanes so a warp scans one list's tree for 32 residual tables at once.
+// ---------------------------------------------------------------------------
+__global__ void ivf_count_kernel(const int32_t* __restrict__ probes, int64_t P, int* cell_cnt, int* pair_pos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < P) pair_pos[i] = atomicAdd(&cell_cnt[probes[i]], 1);
+}
+
+__global__ void __launch_bounds__(1024) ivf_chunks_kernel(const int* __restrict__ cell_cnt, int nlist,
+                                                          const uint32_t* __restrict__ list_leaf_off,
+                                                          int* chunk_off, int* n_chunks, int* chunk_cell,
+                                                          uint32_t* chunk_lo, uint32_t* chunk_hi) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x;
+  const int per = (nlist + blockDim.x - 1) / blockDim.x;
+  const int c0 = min(nlist, t * per), c1 = min(nlist, c0 + per);
+  int loc = 0;
+  for (int c = c0; c < c1; ++c) loc += (cell_cnt[c] + 31) >> 5;
+  part[t] = loc;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {   // Hillis-Steele inclusive scan
+    const int v = (t >= o) ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int run = part[t] - loc;
+  for (int c = c0; c < c1; ++c) {
+    chunk_off[c] = run;
+    const int nc = (cell_cnt[c] + 31) >> 5;
+    for (int j = 0; j < nc; ++j) {
+      chunk_cell[run + j] = c;
+      chunk_lo[run + j] = list_leaf_off[c];
+      chunk_hi[run + j] = list_leaf_off[c + 1];
+    }
+    run += nc;
+  }
+  if (t == blockDim.x - 1) { chunk_off[nlist] = part[t]; *n_chunks = part[t]; }
+}
+
+__global__ void ivf_scatter_kernel(const int32_t* __restrict__ probes, int64_t Q, int w, const int* __restrict__ pair_pos,
+                                   const int* __restrict__ chunk_off, int* chunk_q, int* qslot_off, int* qslot) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < Q * w) {
+    const int c = probes[i];
+    const int p = pair_pos[i];
+    const int ch = chunk_off[c] + (p >> 5);
+    const int ln = p & 31;
+    chunk_q[(size_t)ch * 32 + ln] = (int)(i / w);
+    qslot[i] = ch * 32 + ln;
+  }
+  if (i <= Q) qslot_off[i] = (int)(i * w);
+}
+
+cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist, const uint32_t* list_leaf_off,
+                              int* cell_cnt, int* pair_pos, int* chunk_off, int* n_chunks, int* chunk_cell,
+                              uint32_t* chunk_lo, uint32_t* chunk_hi, int* chunk_q, int max_chunks,
+                              int* qslot_off, int* qslot, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(cell_cnt, 0, (size_t)nlist * 4, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(chunk_q, 0xff, (size_t)max_chunks * 32 * 4, st)) != cudaSuccess) return e;
+  const int64_t P = Q * w;
+  ivf_count_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(probes, P, cell_cnt, pair_pos);
+  ivf_chunks_kernel<<<1, 1024, 0, st>>>(cell_cnt, nlist, list_leaf_off, chunk_off, n_chunks, chunk_cell,
+                                        chunk_lo, chunk_hi);
+  const int64_t n = (P > Q + 1) ? P : Q + 1;
+  ivf_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(probes, Q, w, pair_pos, chunk_off, chunk_q,
+                                                                   qslot_off, qslot);
+  count_launch(3);
+  return cudaGetLastError();
 }
 
 }  // namespace et

@@ -1,0 +1,37 @@
+"""Run a few hot-path steps of one config (for ncu / compute-sanitizer captures).
+
+  python tools/prof_step.py --config c2 --steps 5
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--Q", type=int, default=0)
+    a = ap.parse_args()
+    import torch
+    from paper_1509_05186_b200 import build, synth
+    build.build()
+    cfg = bench.workload_config(a.config)
+    if a.Q:
+        cfg = synth.scaled(cfg, Q=a.Q)
+    dev = torch.device("cuda", 0)
+    st = bench.prepare_ours(cfg, dev, 0, 1)
+    ix = st["ix"]
+    for _ in range(a.steps):
+        d, i = ix.et_etree_topk(cfg.topk, queries=st["q_dev"], codebooks=st["cb_dev"])
+    torch.cuda.synchronize()
+    print("ok", d[0, :4].tolist(), i[0, :4].tolist())
+
+
+if __name__ == "__main__":
+    main()
