@@ -161,11 +161,8 @@ __device__ __forceinline__ float* tab_slot(const SmemScan& sm, float* lut0, int 
 // query slots i = g, g+G, ... read from the staged chunk (broadcast loads).
 template <int NJ>
 __device__ __forceinline__ void build_pass_fixed(const SmemScan& sm, float* lut0, int l, int lv0, int k,
-                                                 bool kvalid, const float* crow, int nq, int g, int G,
+                                                 bool kvalid, const float* c, int nq, int g, int G,
                                                  bool first) {
-  float c[NJ];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) c[j] = kvalid ? __ldg(crow + j) : 0.f;
   int i = g;
   for (; i + G < nq; i += 2 * G) {   // two independent FMA chains
     const float* x0 = sm.stage + i * kDC;
@@ -197,14 +194,14 @@ __device__ __forceinline__ void build_pass_fixed(const SmemScan& sm, float* lut0
 }
 
 __device__ __forceinline__ void build_pass_generic(const SmemScan& sm, float* lut0, int l, int lv0, int k,
-                                                   bool kvalid, const float* crow, int nj, int nq, int g, int G,
+                                                   bool kvalid, const float* c, int nj, int nq, int g, int G,
                                                    bool first) {
   for (int i = g; i < nq; i += G) {
     const float* x0 = sm.stage + i * kDC;
     float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
     float a0 = (!first && kvalid) ? *o0 : 0.f;
     for (int j = 0; j < nj; ++j) {
-      const float t0 = x0[j] - (kvalid ? __ldg(crow + j) : 0.f);
+      const float t0 = x0[j] - c[j];
       a0 = fmaf(t0, t0, a0);
     }
     if (kvalid) *o0 = a0;
@@ -258,31 +255,47 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
     if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * s + j);
     return v;
   };
+  // codeword chunk of pass `pass` for this lane's codeword (registers)
+  const int k = kb * 32 + lane;
+  const bool kvalid = computes && k < K;
+  auto fetch_cw = [&](int pass, float (&c)[kDC]) {
+    const int l = pass / npl, jc = pass - l * npl;
+    const int j0 = jc * kDC;
+    const int nj = min(kDC, s - j0);
+    const int m = p.layer_sub[tr.layer0 + l];
+    const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s + j0;
+#pragma unroll
+    for (int j = 0; j < kDC; ++j) c[j] = (kvalid && j < nj) ? __ldg(crow + j) : 0.f;
+  };
+  float cw[kDC], cwn[kDC];
+  fetch_cw(0, cw);
   float nxt = fetch(0);
   __syncthreads();                              // previous users of the stage are done
   if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
   __syncthreads();
   for (int pass = 0; pass < P; ++pass) {
-    if (pass + 1 < P) nxt = fetch(pass + 1);
+    if (pass + 1 < P) {                         // prefetch the next pass: stage values + codeword chunk
+      nxt = fetch(pass + 1);
+      fetch_cw(pass + 1, cwn);
+    }
     const int l = pass / npl, jc = pass - l * npl;
-    const int j0 = jc * kDC;
-    const int nj = min(kDC, s - j0);
+    const int nj = min(kDC, s - jc * kDC);
     if (computes) {
-      const int k = kb * 32 + lane;
-      const bool kvalid = k < K;
-      const int m = p.layer_sub[tr.layer0 + l];
-      const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s + j0;
       if constexpr (SS > 0 && SS % kDC == 0) {
-        build_pass_fixed<kDC>(sm, lut0, l, lv0, k, kvalid, crow, nq, g, G, jc == 0);
+        build_pass_fixed<kDC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
       } else if constexpr (SS > 0) {
-        if (nj == kDC) build_pass_fixed<kDC>(sm, lut0, l, lv0, k, kvalid, crow, nq, g, G, jc == 0);
-        else build_pass_fixed<(SS % kDC) ? (SS % kDC) : kDC>(sm, lut0, l, lv0, k, kvalid, crow, nq, g, G, jc == 0);
+        if (nj == kDC) build_pass_fixed<kDC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
+        else build_pass_fixed<(SS % kDC) ? (SS % kDC) : kDC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
       } else {
-        build_pass_generic(sm, lut0, l, lv0, k, kvalid, crow, nj, nq, g, G, jc == 0);
+        build_pass_generic(sm, lut0, l, lv0, k, kvalid, cw, nj, nq, g, G, jc == 0);
       }
     }
     __syncthreads();
-    if (pass + 1 < P && threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
+    if (pass + 1 < P) {
+      if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
+#pragma unroll
+      for (int j = 0; j < kDC; ++j) cw[j] = cwn[j];
+    }
     __syncthreads();
   }
 }
@@ -387,30 +400,46 @@ struct EmitCtx {
   TopkState ts;
 };
 
+// Append one group's distance to this lane's candidates if it can still be in
+// the top-k (hot path: no calls, no syncs).  Buffers are pruned at batch
+// boundaries by maybe_refresh, which keeps >= 32 free slots per lane.
 __device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, uint32_t mult) {
   const ScanParams& p = *e.p;
-  const int lane = lane_id();
   if (p.mode == kModeFull) {
-    p.leafdist[((size_t)e.chunk * p.n_groups + g) * 32 + lane] = dist;
+    p.leafdist[((size_t)e.chunk * p.n_groups + g) * 32 + lane_id()] = dist;
     return;
   }
   TopkState& ts = e.ts;
-  const bool pass = ts.active && dist <= ts.thr;
-  if (__any_sync(FULLMASK, pass)) {
-    if (pass) {
-      ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), g);
-      ++ts.cnt;
-      if (mult >= (uint32_t)p.k) ts.thr = dist;   // one group alone bounds the k-th distance
-    }
-    unsigned full = __ballot_sync(FULLMASK, ts.cnt >= p.B);
-    while (full) {
-      const int L = __ffs(full) - 1;
-      full &= full - 1;
-      int nc; float nt;
-      const int n = __shfl_sync(FULLMASK, ts.cnt, L);
-      refresh_buffer(ts.warp_buf + (size_t)L * p.B, n, p.k, p.group_mult, p.group_minid, &nc, &nt);
-      if (lane == L) { ts.cnt = nc; ts.thr = fminf(ts.thr, nt); }
-    }
+  if (ts.active && dist <= ts.thr) {
+    ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), g);
+    ++ts.cnt;
+    if (mult >= (uint32_t)p.k) ts.thr = dist;   // one group alone bounds the k-th distance
+  }
+}
+
+struct CntThr { int cnt; float thr; };
+
+__device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr, int B, int k,
+                                             const uint32_t* gmult, const int32_t* gminid) {
+  const int lane = lane_id();
+  unsigned full = __ballot_sync(FULLMASK, cnt > B - 32);
+  while (full) {
+    const int L = __ffs(full) - 1;
+    full &= full - 1;
+    int nc; float nt;
+    const int n = __shfl_sync(FULLMASK, cnt, L);
+    refresh_buffer(warp_buf + (size_t)L * B, n, k, gmult, gminid, &nc, &nt);
+    if (lane == L) { cnt = nc; thr = fminf(thr, nt); }
+  }
+  return CntThr{cnt, thr};
+}
+
+__device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
+  const ScanParams& p = *e.p;
+  if (__any_sync(FULLMASK, e.ts.cnt > p.B - 32)) {
+    const CntThr r = maybe_refresh(e.ts.warp_buf, e.ts.cnt, e.ts.thr, p.B, p.k, p.group_mult, p.group_minid);
+    e.ts.cnt = r.cnt;
+    e.ts.thr = r.thr;
   }
 }
 
@@ -418,7 +447,7 @@ __device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, u
 // internal levels, P:239-243 for the leaf and its postfix): ctx[l] =
 // ctx[l-1] + T[l][code byte l], summed left to right exactly like naive ADC.
 // All lookups of the leaf are issued before the (dependent) additions.
-template <int MT>
+template <int MT, int ROLE>
 __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b,
                           const float* lut0g) {
   const ScanParams& p = *e.p;
@@ -436,8 +465,8 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
     const uint64_t mycode = in ? __ldg(tr.code + idx) : 0ull;
     const uint32_t mylcp = in ? (uint32_t)__ldg(tr.lcp + idx) : 0u;
     uint32_t aux0 = 0, aux1 = 0;   // role 1: multiplicity; role 2: tuple range
-    if (e.role == 1 && topk && in) aux0 = __ldg(p.group_mult + idx);
-    if (e.role == 2 && in) { aux0 = __ldg(p.t0_tup_off + idx); aux1 = __ldg(p.t0_tup_off + idx + 1); }
+    if (ROLE == 1 && topk && in) aux0 = __ldg(p.group_mult + idx);
+    if (ROLE == 2 && in) { aux0 = __ldg(p.t0_tup_off + idx); aux1 = __ldg(p.t0_tup_off + idx + 1); }
     const int n = (int)min(32u, b - base);
     for (int j = 0; j < n; ++j) {
       const uint32_t lo = __shfl_sync(FULLMASK, (uint32_t)mycode, j);
@@ -457,15 +486,16 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
         if (l >= pl) ctx[l] = (l == 0) ? v[0] : ctx[l > 0 ? l - 1 : 0] + v[l];
       const float dist = ctx[MT - 1];
       const uint32_t leaf = base + j;
-      if (e.role == 0) {
+      if constexpr (ROLE == 0) {
         e.part[(size_t)p.part_base[e.t] + (size_t)leaf * 32 + lane] = dist;
-      } else if (e.role == 1) {
+      } else if constexpr (ROLE == 1) {
         const uint32_t mult = __shfl_sync(FULLMASK, aux0, j);
         emit_group(e, dist, leaf, mult);
       } else {
         const uint32_t t0 = __shfl_sync(FULLMASK, aux0, j);
         const uint32_t t1 = __shfl_sync(FULLMASK, aux1, j);
         for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
+          if (topk && ((g - t0) & 31) == 31) refresh_if_needed(e);
           float dd = dist;
           for (int tt = 1; tt < p.T; ++tt) {
             const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
@@ -476,7 +506,8 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
         }
       }
     }
-    if (topk && e.role != 0) {   // share the threshold with the CTA's other warps
+    if (topk && ROLE != 0) {   // prune full buffers; share the threshold with the CTA's other warps
+      refresh_if_needed(e);
       if (e.ts.active) {
         atomicMin(&sm.thr[lane], __float_as_uint(e.ts.thr));
         e.ts.thr = __uint_as_float(*((volatile unsigned*)&sm.thr[lane]));
@@ -485,23 +516,32 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
   }
 }
 
+template <int ROLE>
 __device__ __forceinline__ void scan_dispatch(EmitCtx& e, const SmemScan& sm, const TreeDev& tr,
                                               uint32_t a, uint32_t b, const float* lut0g) {
   switch (tr.MT) {
-    case 1: scan_tree<1>(e, sm, tr, a, b, lut0g); break;
-    case 2: scan_tree<2>(e, sm, tr, a, b, lut0g); break;
-    case 3: scan_tree<3>(e, sm, tr, a, b, lut0g); break;
-    case 4: scan_tree<4>(e, sm, tr, a, b, lut0g); break;
-    case 5: scan_tree<5>(e, sm, tr, a, b, lut0g); break;
-    case 6: scan_tree<6>(e, sm, tr, a, b, lut0g); break;
-    case 7: scan_tree<7>(e, sm, tr, a, b, lut0g); break;
-    case 8: scan_tree<8>(e, sm, tr, a, b, lut0g); break;
+    case 1: scan_tree<1, ROLE>(e, sm, tr, a, b, lut0g); break;
+    case 2: scan_tree<2, ROLE>(e, sm, tr, a, b, lut0g); break;
+    case 3: scan_tree<3, ROLE>(e, sm, tr, a, b, lut0g); break;
+    case 4: scan_tree<4, ROLE>(e, sm, tr, a, b, lut0g); break;
+    case 5: scan_tree<5, ROLE>(e, sm, tr, a, b, lut0g); break;
+    case 6: scan_tree<6, ROLE>(e, sm, tr, a, b, lut0g); break;
+    case 7: scan_tree<7, ROLE>(e, sm, tr, a, b, lut0g); break;
+    case 8: scan_tree<8, ROLE>(e, sm, tr, a, b, lut0g); break;
     default: break;
   }
 }
 
-template <int SS>
-__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanParams p) {
+// MTC > 0: every tree has MTC levels (compile time); 0: runtime switch.
+template <int MTC, int ROLE>
+__device__ __forceinline__ void scan_any(EmitCtx& e, const SmemScan& sm, const TreeDev& tr,
+                                         uint32_t a, uint32_t b, const float* lut0g) {
+  if constexpr (MTC > 0) scan_tree<MTC, ROLE>(e, sm, tr, a, b, lut0g);
+  else scan_dispatch<ROLE>(e, sm, tr, a, b, lut0g);
+}
+
+template <int SS, int MTC, bool FOREST>
+__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int unit = blockIdx.x;
   const int chunk = unit / p.S;
@@ -563,8 +603,14 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const ScanParams p) {
     const uint32_t wa = lo + (uint32_t)(((uint64_t)len * warp) / kWarps);
     const uint32_t wb = lo + (uint32_t)(((uint64_t)len * (warp + 1)) / kWarps);
     e.t = t;
-    e.role = (t > 0) ? 0 : (p.T == 1 ? 1 : 2);
-    if (wa < wb) scan_dispatch(e, sm, tr, wa, wb, lut0g);
+    if (wa < wb) {
+      if constexpr (FOREST) {
+        if (t > 0) scan_any<MTC, 0>(e, sm, tr, wa, wb, lut0g);
+        else scan_any<MTC, 2>(e, sm, tr, wa, wb, lut0g);
+      } else {
+        scan_any<MTC, 1>(e, sm, tr, wa, wb, lut0g);
+      }
+    }
     __syncthreads();   // partials visible / tables free for the next tree
   }
 
@@ -579,13 +625,25 @@ size_t scan_smem_bytes(int MTmax) {
   return (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + 32 * kDC * 4;
 }
 
-template <int SS>
+template <int SS, int MTC, bool FOREST>
 static cudaError_t launch_scan_t(const ScanParams& p, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS, MTC, FOREST>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  scan_kernel<SS><<<p.n_units, kThreads, smem, st>>>(p);
+  scan_kernel<SS, MTC, FOREST><<<p.n_units, kThreads, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int SS>
+static cudaError_t launch_scan_s(const ScanParams& p, size_t smem, cudaStream_t st) {
+  bool uni = true;
+  for (int t = 1; t < p.T; ++t) uni = uni && (p.tree[t].MT == p.tree[0].MT);
+  const int mt = uni ? p.tree[0].MT : 0;
+  const bool forest = p.T > 1;
+  if (mt == 8) return forest ? launch_scan_t<SS, 8, true>(p, smem, st) : launch_scan_t<SS, 8, false>(p, smem, st);
+  if (mt == 4) return forest ? launch_scan_t<SS, 4, true>(p, smem, st) : launch_scan_t<SS, 4, false>(p, smem, st);
+  return forest ? launch_scan_t<SS, 0, true>(p, smem, st) : launch_scan_t<SS, 0, false>(p, smem, st);
 }
 
 cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st) {
@@ -593,12 +651,9 @@ cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st) {
   const size_t smem = scan_smem_bytes(MTmax);
   const bool v4 = (p.luts == nullptr) && (p.d % 4 == 0) && p.vec4;
   switch (v4 ? p.s : 0) {
-    case 4: return launch_scan_t<4>(p, smem, st);
-    case 8: return launch_scan_t<8>(p, smem, st);
-    case 16: return launch_scan_t<16>(p, smem, st);
-    case 32: return launch_scan_t<32>(p, smem, st);
-    case 60: return launch_scan_t<60>(p, smem, st);
-    default: return launch_scan_t<0>(p, smem, st);
+    case 16: return launch_scan_s<16>(p, smem, st);
+    case 60: return launch_scan_s<60>(p, smem, st);
+    default: return launch_scan_s<0>(p, smem, st);
   }
 }
 
@@ -675,7 +730,7 @@ struct CandSrc {
   }
 };
 
-__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const FinParams p) {
+__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_constant__ FinParams p) {
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   FinSmem& fs = *reinterpret_cast<FinSmem*>(fsm_raw);
   const float* unit_thr = p.unit_thr;
