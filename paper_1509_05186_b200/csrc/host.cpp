@@ -886,9 +886,8 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   Carve c{reinterpret_cast<char*>(workspace), 0, ws};
   Work w = carve(c, ix, pl, Q, false, 1);
   cudaStream_t st = (cudaStream_t)stream;
-  cuda_check(timed("fill", st, [&] { return launch_fill_flat(Q, pl.n_chunks, w.chunk_q, w.qslot_off, w.qslot, st); }), "fill");
   fill_scan_common(sp, ix, pl);
-  sp.chunk_q = w.chunk_q;
+  sp.flatQ = Q;   // arithmetic chunking: no fill launch
   sp.lut0 = w.lut0;
   sp.partials = w.partials;
   sp.mode = kModeTopk;
@@ -900,7 +899,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
-  fp.qslot_off = w.qslot_off; fp.qslot = w.qslot;
+  fp.flat_nchunks = pl.n_chunks;
   fp.cand = w.cand; fp.cand_cnt = w.cand_cnt;
   fp.group_off = ix->group_off.as<uint32_t>();
   fp.ids = ix->ids.as<int32_t>();

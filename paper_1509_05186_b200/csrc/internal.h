@@ -43,6 +43,7 @@ struct ScanParams {
   int n_units = 0;                    // CTAs = n_chunks * S
   int S = 1;                          // leaf segments per chunk
   const int* chunk_q = nullptr;       // [n_chunks][32] query of each lane, -1 = idle (active lanes first)
+  int64_t flatQ = 0;                  // > 0: chunk c holds queries [c*Q/n, (c+1)*Q/n) (chunk_q unused)
   const int* chunk_cell = nullptr;    // [n_chunks] coarse cell (IVF) or null
   const uint32_t* chunk_lo = nullptr; // [n_chunks] tree-0 leaf range (IVF lists) or null
   const uint32_t* chunk_hi = nullptr;
@@ -76,6 +77,7 @@ struct FinParams {
   int k = 0, B = 0, S = 1;
   const int* qslot_off = nullptr;     // [Q+1]
   const int* qslot = nullptr;         // chunk*32 + lane for each (query, probe)
+  int flat_nchunks = 0;               // > 0: one slot per query, computed from the flat chunking
   const uint2* cand = nullptr;
   const int* cand_cnt = nullptr;
   const uint32_t* group_off = nullptr;  // [n_groups+1]

@@ -147,7 +147,62 @@ struct SmemScan {
   unsigned* thr;       // [32] CTA-shared top-k thresholds (float bits)
   int* qidx;           // [32] query of each lane
   float* stage;        // [32 queries][kDC dims] query sub-vector chunk (table build)
+  uint32_t* tmem_slot; // TMEM base address written by tcgen05.alloc
+  uint32_t tmem;       // TMEM base (level-0 tables of 8-level trees), 0 if unused
 };
+
+// ---------------------------------------------------------------------------
+// Tensor Memory (TMEM) as a lookup-table store.  An 8-level tree needs 8
+// tables of 32 KB for the CTA's 32 queries but shared memory holds 7; level 0
+// lives in TMEM: 256 columns x 32 lanes (lane = query), one copy per warp
+// quadrant (a warp may only address its own 32 TMEM lanes), read with
+// tcgen05.ld.32x32b.x1 by warp-uniform column = codeword.
+// ---------------------------------------------------------------------------
+constexpr int kTmemCols = 256;
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(slot);
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(a), "r"(kTmemCols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(base), "r"(kTmemCols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ uint32_t tmem_lane_base(uint32_t base) {
+  return base + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);   // this warp's 32-lane quadrant
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                  "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                  "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])) : "memory");
+}
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t x;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(x) : "r"(taddr));
+  return x;
+}
+__device__ __forceinline__ void tmem_wait_ld(uint32_t& x) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(x));
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Copy the level-0 table (global scratch row [256][32], just built by this CTA)
+// into each warp quadrant's TMEM lanes: warp w copies 64 columns for quadrant w&3.
+__device__ void tmem_load_level0(const SmemScan& sm, const float* lut0) {
+  const int lane = lane_id(), warp = warp_id();
+  const int sub = warp >> 2;               // 4 warps per quadrant
+  const uint32_t tb = tmem_lane_base(sm.tmem);
+  for (int c0 = sub * 64; c0 < sub * 64 + 64; c0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = lut0[(c0 + j) * 32 + lane];
+    tmem_st8(tb + (uint32_t)c0, v);
+  }
+  tmem_wait_st();
+}
 
 constexpr int kDC = 16;   // query dimensions staged per table-build pass
 
@@ -206,6 +261,88 @@ __device__ __forceinline__ void build_pass_generic(const SmemScan& sm, float* lu
     }
     if (kvalid) *o0 = a0;
   }
+}
+
+// Resident-staging build for s == 16 (every d = 128 configuration): the
+// active queries' sub-vectors of levels 0..MT-2 are staged once into the
+// shared-memory region of the tree's LAST level (not built yet), those levels
+// are built without barriers, then the last level is built from the small
+// stage.  Three barriers per tree instead of two per pass.
+template <int SS>
+__device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq,
+                                      int cell) {
+  static_assert(SS == kDC, "resident staging handles s == 16");
+  const TreeDev& tr = p.tree[t];
+  const int MT = tr.MT;
+  const int lv0 = (MT == 8) ? 1 : 0;
+  const int K = p.K, d = p.d;
+  const int nb = (K + 31) >> 5;
+  const int lane = lane_id(), warp = warp_id();
+  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
+  float* region = sm.tab + (size_t)(MT - 1 - lv0) * 256 * 32;   // last level's table region
+  // ---- stage: levels 0..MT-2 -> region [l][i][16]; level MT-1 -> sm.stage [i][16]
+  const int per_level = nq * SS;
+  const int total = MT * per_level;
+  __syncthreads();                                   // previous tree's scan is done with the tables
+  for (int e = threadIdx.x; e < total; e += kThreads) {
+    const int l = e / per_level, r = e - l * per_level;
+    const int i = r / SS, j = r - i * SS;
+    const int m = p.layer_sub[tr.layer0 + l];
+    const int q = sm.qidx[i];
+    float v = __ldg(p.queries + (size_t)q * d + (size_t)m * SS + j);
+    if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * SS + j);
+    if (l < MT - 1) region[e] = v;
+    else sm.stage[r] = v;
+  }
+  __syncthreads();
+  const int G = max(1, kWarps / nb);
+  auto item = [&](int l, int kb, int g, const float* xs, int xstride) {
+    const int k = kb * 32 + lane;
+    const bool kvalid = k < K;
+    const int m = p.layer_sub[tr.layer0 + l];
+    const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
+    float c[SS];
+#pragma unroll
+    for (int j = 0; j < SS; j += 4) {
+      const float4 v = kvalid ? __ldg(reinterpret_cast<const float4*>(crow + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
+    }
+    int i = g;
+    for (; i + G < nq; i += 2 * G) {
+      const float* x0 = xs + i * xstride;
+      const float* x1 = xs + (i + G) * xstride;
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < SS; ++j) {
+        const float t0 = x0[j] - c[j];
+        const float t1 = x1[j] - c[j];
+        a0 = fmaf(t0, t0, a0);
+        a1 = fmaf(t1, t1, a1);
+      }
+      if (kvalid) {
+        *tab_slot(sm, lut0, l, lv0, k, i) = a0;
+        *tab_slot(sm, lut0, l, lv0, k, i + G) = a1;
+      }
+    }
+    if (i < nq) {
+      const float* x0 = xs + i * xstride;
+      float a0 = 0.f;
+#pragma unroll
+      for (int j = 0; j < SS; ++j) {
+        const float t0 = x0[j] - c[j];
+        a0 = fmaf(t0, t0, a0);
+      }
+      if (kvalid) *tab_slot(sm, lut0, l, lv0, k, i) = a0;
+    }
+  };
+  const int per = nb * G;
+  for (int it = warp; it < (MT - 1) * per; it += kWarps) {
+    const int l = it / per, r = it - l * per;
+    item(l, r % nb, r / nb, region + (size_t)l * per_level, SS);
+  }
+  __syncthreads();                                   // region free: build the last level into it
+  for (int it = warp; it < per; it += kWarps) item(MT - 1, it % nb, it / nb, sm.stage, SS);
+  __syncthreads();
 }
 
 // Build the tables of tree t for this CTA's queries (fused).
@@ -454,6 +591,7 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
   constexpr int lv0 = (MT == 8) ? 1 : 0;
   const int lane = lane_id();
   const float* tab = sm.tab;
+  const uint32_t tq = tmem_lane_base(sm.tmem);
   float ctx[MT];
 #pragma unroll
   for (int l = 0; l < MT; ++l) ctx[l] = 0.f;
@@ -474,12 +612,18 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
       int pl = (int)__shfl_sync(FULLMASK, mylcp, j);
       if (base + j == a) pl = 0;   // first leaf of this warp's range: rebuild the whole path
       float v[MT];
+      uint32_t v0t = 0;
 #pragma unroll
       for (int l = 0; l < MT; ++l) {
         if (l >= pl) {
           const uint32_t kb = ((l < 4 ? lo : hi) >> (8 * (l & 3))) & 255u;
-          v[l] = (l < lv0) ? lut0g[kb * 32 + lane] : tab[tab_index(l - lv0, kb, lane)];
+          if (l < lv0) v0t = tmem_ld1(tq + kb);
+          else v[l] = tab[tab_index(l - lv0, kb, lane)];
         }
+      }
+      if (lv0 > 0 && pl == 0) {
+        tmem_wait_ld(v0t);
+        v[0] = __uint_as_float(v0t);
       }
 #pragma unroll
       for (int l = 0; l < MT; ++l)
@@ -556,12 +700,29 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   sm.thr = reinterpret_cast<unsigned*>(smem_raw + (size_t)smem_levels * 256 * 32 * 4);
   sm.qidx = reinterpret_cast<int*>(sm.thr + 32);
   sm.stage = reinterpret_cast<float*>(sm.qidx + 32);
+  sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.stage + 32 * kDC);
+  sm.tmem = 0;
+  const bool use_tmem = (MTmax == 8);
+  if (use_tmem) {
+    if (warp == 0) tmem_alloc(sm.tmem_slot);
+    tmem_fence_before();
+  }
 
   if (threadIdx.x < 32) {
-    sm.qidx[lane] = __ldg(p.chunk_q + (size_t)chunk * 32 + lane);
+    if (p.flatQ > 0) {
+      const int nch = p.n_units / p.S;
+      const int64_t s0 = (int64_t)chunk * p.flatQ / nch, s1 = (int64_t)(chunk + 1) * p.flatQ / nch;
+      sm.qidx[lane] = (s0 + lane < s1) ? (int)(s0 + lane) : -1;
+    } else {
+      sm.qidx[lane] = __ldg(p.chunk_q + (size_t)chunk * 32 + lane);
+    }
     sm.thr[lane] = 0x7f800000u;   // +inf
   }
   __syncthreads();
+  if (use_tmem) {
+    tmem_fence_after();
+    sm.tmem = *sm.tmem_slot;
+  }
   int nq = 0;
   {
     const int q = sm.qidx[lane];
@@ -589,8 +750,20 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   // then tree 0, whose leaves walk their tuples and sum in tree order.
   for (int t = p.T - 1; t >= 0; --t) {
     const TreeDev& tr = p.tree[t];
-    build_tables<SS>(p, sm, t, unit, nq, cell);
-    __syncthreads();
+    if constexpr (SS == kDC) {
+      if (p.luts) { build_tables<SS>(p, sm, t, unit, nq, cell); __syncthreads(); }
+      else build_tables_resident<SS>(p, sm, t, unit, nq, cell);
+    } else {
+      build_tables<SS>(p, sm, t, unit, nq, cell);
+      __syncthreads();
+    }
+    if (tr.MT == 8) {   // level 0 -> TMEM (every warp copies a quarter of its quadrant's columns)
+      tmem_fence_after();
+      tmem_load_level0(sm, lut0g);
+      tmem_fence_before();
+      __syncthreads();
+      tmem_fence_after();
+    }
     uint32_t lo = 0, hi = (uint32_t)tr.n_leaves;
     if (t == 0) {
       if (p.chunk_lo) { lo = __ldg(p.chunk_lo + chunk); hi = __ldg(p.chunk_hi + chunk); }
@@ -611,8 +784,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
         scan_any<MTC, 1>(e, sm, tr, wa, wb, lut0g);
       }
     }
+    tmem_fence_before();
     __syncthreads();   // partials visible / tables free for the next tree
+    tmem_fence_after();
   }
+  if (use_tmem && warp == 0) tmem_dealloc(sm.tmem);
 
   if (p.mode == kModeTopk) {
     p.cand_cnt[(size_t)(unit * kWarps + warp) * 32 + lane] = e.ts.cnt;
@@ -622,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
 
 size_t scan_smem_bytes(int MTmax) {
   const int levels = (MTmax == 8) ? 7 : MTmax;
-  return (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + 32 * kDC * 4;
+  return (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + 32 * kDC * 4 + 16;
 }
 
 template <int SS, int MTC, bool FOREST>
@@ -666,10 +842,10 @@ __device__ void warp_bitonic_sort(unsigned long long* a, int n) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncwarp();
       for (int i = lane; i < n / 2; i += 32) {
-        const int lo = 2 * stride * (i / stride) + (i % stride);
+        const int lo = ((i & ~(stride - 1)) << 1) | (i & (stride - 1));   // stride is a power of two
         const int hi = lo + stride;
         const bool up = ((lo & size) == 0);
-        unsigned long long x = a[lo], y = a[hi];
+        const unsigned long long x = a[lo], y = a[hi];
         if ((x > y) == up) { a[lo] = y; a[hi] = x; }
       }
     }
@@ -692,10 +868,26 @@ struct FinSmem {
   uint32_t tied_g[kFinWarps];
 };
 
+// Slots (chunk*32 + lane) of query q: explicit (IVF: one per probe) or, for the
+// flat plan, the query's position in the arithmetic chunking.
+__device__ __forceinline__ int fin_s0(const FinParams& p, int64_t q) { return p.flat_nchunks ? 0 : p.qslot_off[q]; }
+__device__ __forceinline__ int fin_s1(const FinParams& p, int64_t q) { return p.flat_nchunks ? 1 : p.qslot_off[q + 1]; }
+__device__ __forceinline__ int fin_slot(const FinParams& p, int64_t q, int j) {
+  if (p.flat_nchunks) {
+    const int64_t n = p.flat_nchunks, Q = p.Q;
+    int64_t c = q * n / Q;
+    while (c + 1 < n && (c + 1) * Q / n <= q) ++c;
+    while (c > 0 && c * Q / n > q) --c;
+    return (int)(c * 32 + (q - c * Q / n));
+  }
+  return __ldg(p.qslot + j);
+}
+
 // Enumerates the candidates of query q: smem copy when they fit, else global.
 // f(key, group, multiplicity) is called once per candidate by the owning lane.
 struct CandSrc {
   const FinParams* p;
+  int64_t q;
   int s0, s1;
   bool in_smem;
   int n;               // staged count (smem)
@@ -712,7 +904,7 @@ struct CandSrc {
     }
     const uint32_t tb = __float_as_uint(thr);
     for (int j = s0; j < s1; ++j) {
-      const int slot = __ldg(p->qslot + j);
+      const int slot = fin_slot(*p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
       for (int sg = 0; sg < p->S; ++sg) {
         const int unit = chunk * p->S + sg;
@@ -738,13 +930,13 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   const int64_t q = (int64_t)blockIdx.x * kFinWarps + warp;
   if (q >= p.Q) return;
   const int k = p.k;
-  const int s0 = p.qslot_off[q], s1 = p.qslot_off[q + 1];
+  const int s0 = fin_s0(p, q), s1 = fin_s1(p, q);
 
   // 1. threshold prefilter: min over the query's units of their final thresholds
   float thr = __int_as_float(0x7f800000);
   if (unit_thr) {
     for (int j = s0; j < s1; ++j) {
-      const int slot = __ldg(p.qslot + j);
+      const int slot = fin_slot(p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
       for (int sg = lane; sg < p.S; sg += 32)
         thr = fminf(thr, __ldg(unit_thr + (size_t)(chunk * p.S + sg) * 32 + ln));
@@ -761,7 +953,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
     uint32_t* G_ = fs.grp[warp];
     uint32_t* U_ = fs.mul[warp];
     for (int j = s0; j < s1 && !overflow; ++j) {
-      const int slot = __ldg(p.qslot + j);
+      const int slot = fin_slot(p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
       for (int sg = 0; sg < p.S && !overflow; ++sg) {
         const int unit = chunk * p.S + sg;
@@ -799,7 +991,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   }
   __syncwarp();
   CandSrc src;
-  src.p = &p; src.s0 = s0; src.s1 = s1; src.in_smem = !overflow; src.n = n;
+  src.p = &p; src.q = q; src.s0 = s0; src.s1 = s1; src.in_smem = !overflow; src.n = n;
   src.key = fs.key[warp]; src.grp = fs.grp[warp]; src.mul = fs.mul[warp]; src.thr = thr;
 
   // 3. weighted radix select: t = smallest distance with cumulative multiplicity >= k
