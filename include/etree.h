@@ -88,6 +88,14 @@ et_status et_build_codebooks(const float* train, int64_t n, int32_t d, int32_t M
                              int32_t K, int32_t lloyd_iters, uint64_t seed,
                              float* codebooks, double* objective_hist);
 
+/* Coarse quantizer for IVF ("K'"): k-means++ seeding from `seed`
+ * then `lloyd_iters` Lloyd iterations over full d-dimensional vectors.
+ * train: HOST fp32 [n][d]; centroids: HOST fp32 [nlist][d] (written);
+ * objective_hist: optional HOST double [lloyd_iters].  1 <= nlist <= 65536. */
+et_status et_build_coarse(const float* train, int64_t n, int32_t d, int32_t nlist,
+                          int32_t lloyd_iters, uint64_t seed, float* centroids,
+                          double* objective_hist);
+
 /* Encode: code byte m = argmin_k ||x_m - c_m(k)||^2, fp32 direct difference,
  * ties -> lowest k.  codebooks, x: DEVICE; codes: DEVICE uint8 [n][M].
  * centroids/assign optional (both DEVICE, may be NULL): if given, the residual

@@ -51,6 +51,7 @@ SIGNATURES = [
     ("et_timing_reset", None, []),
     ("et_timing_get", C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(I64)]),
     ("et_build_codebooks", C.c_int, [P, I64, I32, I32, I32, I32, U64, P, P]),
+    ("et_build_coarse", C.c_int, [P, I64, I32, I32, I32, U64, P, P]),
     ("et_encode", C.c_int, [P, I32, I32, I32, P, I64, P, P, P, P]),
     ("et_assign", C.c_int, [P, I32, I32, P, I64, P, P]),
     ("et_build_etree", C.c_int, [P, P, I64, I32, I32, P, C.POINTER(P)]),

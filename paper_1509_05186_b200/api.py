@@ -275,6 +275,17 @@ def et_build_stats(codes, split=None, ids=None, K: int = 256, byte_perm=None):
     return [out[t].as_dict() for t in range(T)]
 
 
+def et_build_coarse(train, nlist: int, lloyd_iters: int, seed: int):
+    """Host fp32 [n, d] -> (centroids [nlist, d] float32, objective history [iters])."""
+    train = _host(train, np.float32)
+    n, d = train.shape
+    c = np.empty((nlist, d), dtype=np.float32)
+    hist = np.empty((lloyd_iters,), dtype=np.float64)
+    check(_lib.load().et_build_coarse(_ptr(train), n, d, nlist, lloyd_iters, seed & (2**64 - 1),
+                                      _ptr(c), _ptr(hist)))
+    return c, hist
+
+
 def et_merge_topk(dist, ids, stream=None):
     """dist/ids [G, Q, k] (e.g. all-gathered shards) -> merged [Q, k]."""
     torch = _t()

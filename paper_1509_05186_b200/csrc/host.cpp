@@ -1142,3 +1142,118 @@ extern "C" et_status et_build_codebooks(const float* train, int64_t n, int32_t d
   cleanup();
   ET_API_END
 }
+
+// ---------------------------------------------------------------------------
+// coarse quantizer for IVF (K' up to 65536 centroids of full dimension d):
+// k-means++ on the host (fp64; distance updates split over threads), Lloyd
+// with the GPU assign kernel, fp64 centroid updates, empty -> farthest point.
+// ---------------------------------------------------------------------------
+extern "C" et_status et_build_coarse(const float* train, int64_t n, int32_t d, int32_t nlist, int32_t lloyd_iters,
+                                     uint64_t seed, float* centroids, double* objective_hist) {
+  ET_API_BEGIN
+  if (!train || !centroids) fail(ET_ERR_CONFIG, "null argument");
+  if (d <= 0 || nlist <= 0 || nlist > 65536) fail(ET_ERR_CONFIG, "bad d / nlist");
+  if (n < nlist) fail(ET_ERR_INSUFFICIENT_DATA, "n < nlist");
+  if (lloyd_iters < 1) fail(ET_ERR_CONFIG, "lloyd_iters >= 1");
+  if ((size_t)32 * d * 4 > 200 * 1024) fail(ET_ERR_CONFIG, "d too large");
+  for (int64_t i = 0; i < n * d; ++i)
+    if (!std::isfinite(train[i])) fail(ET_ERR_INVALID_VECTOR, "non-finite training value");
+  std::vector<double> C((size_t)nlist * d);
+  {
+    uint64_t rs = seed * 1000003ull + 77;
+    std::vector<double> D(n);
+    const int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    auto update = [&](const double* c, bool first) {
+      std::vector<std::thread> th;
+      std::vector<double> part(nth, 0.0);
+      for (int w = 0; w < nth; ++w)
+        th.emplace_back([&, w]() {
+          const int64_t a = n * w / nth, b = n * (w + 1) / nth;
+          double acc = 0;
+          for (int64_t i = a; i < b; ++i) {
+            const float* x = train + (size_t)i * d;
+            double s2 = 0;
+            for (int j = 0; j < d; ++j) { const double t = (double)x[j] - c[j]; s2 += t * t; }
+            D[i] = first ? s2 : std::min(D[i], s2);
+            acc += D[i];
+          }
+          part[w] = acc;
+        });
+      for (auto& t : th) t.join();
+      double tot = 0;
+      for (double v : part) tot += v;
+      return tot;
+    };
+    int64_t i0 = (int64_t)(splitmix64(rs) % (uint64_t)n);
+    for (int j = 0; j < d; ++j) C[j] = train[(size_t)i0 * d + j];
+    double tot = update(C.data(), true);
+    for (int k = 1; k < nlist; ++k) {
+      int64_t pick = n - 1;
+      if (tot <= 0) pick = (int64_t)(splitmix64(rs) % (uint64_t)n);
+      else {
+        const double u = u01(rs) * tot;
+        double acc = 0;
+        for (int64_t i = 0; i < n; ++i) { acc += D[i]; if (acc > u) { pick = i; break; } }
+      }
+      double* ck = C.data() + (size_t)k * d;
+      for (int j = 0; j < d; ++j) ck[j] = train[(size_t)pick * d + j];
+      tot = update(ck, false);
+    }
+  }
+  float* dx = nullptr; float* dc = nullptr; int32_t* da = nullptr; float* dd = nullptr;
+  auto cleanup = [&]() { if (dx) cudaFree(dx); if (dc) cudaFree(dc); if (da) cudaFree(da); if (dd) cudaFree(dd); };
+  try {
+    cuda_check(cudaMalloc(&dx, (size_t)n * d * 4), "cudaMalloc(train)");
+    cuda_check(cudaMalloc(&dc, (size_t)nlist * d * 4), "cudaMalloc(centroids)");
+    cuda_check(cudaMalloc(&da, (size_t)n * 4), "cudaMalloc(assign)");
+    cuda_check(cudaMalloc(&dd, (size_t)n * 4), "cudaMalloc(dist)");
+    cuda_check(cudaMemcpy(dx, train, (size_t)n * d * 4, cudaMemcpyHostToDevice), "upload train");
+    std::vector<float> Cf((size_t)nlist * d);
+    std::vector<int32_t> a(n);
+    for (int it = 0; it < lloyd_iters; ++it) {
+      for (size_t i = 0; i < Cf.size(); ++i) Cf[i] = (float)C[i];
+      cuda_check(cudaMemcpy(dc, Cf.data(), Cf.size() * 4, cudaMemcpyHostToDevice), "upload centroids");
+      cuda_check(launch_assign(dc, nlist, d, dx, n, da, dd, 0), "assign");
+      cuda_check(cudaMemcpy(a.data(), da, (size_t)n * 4, cudaMemcpyDeviceToHost), "download assign");
+      std::vector<double> sum((size_t)nlist * d, 0.0), far(n);
+      std::vector<int64_t> cnt(nlist, 0);
+      double obj = 0;
+      for (int64_t i = 0; i < n; ++i) {
+        const int k = a[i];
+        const float* x = train + (size_t)i * d;
+        double s2 = 0;
+        for (int j = 0; j < d; ++j) {
+          const double t = (double)x[j] - (double)Cf[(size_t)k * d + j];
+          s2 += t * t;
+          sum[(size_t)k * d + j] += x[j];
+        }
+        far[i] = s2;
+        obj += s2;
+        ++cnt[k];
+      }
+      if (objective_hist) objective_hist[it] = obj;
+      std::vector<int64_t> order;
+      size_t next_far = 0;
+      for (int k = 0; k < nlist; ++k) {
+        double* ck = C.data() + (size_t)k * d;
+        if (cnt[k] > 0) {
+          for (int j = 0; j < d; ++j) ck[j] = sum[(size_t)k * d + j] / (double)cnt[k];
+        } else {
+          if (order.empty()) {
+            order.resize(n);
+            std::iota(order.begin(), order.end(), 0);
+            std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return far[x] > far[y]; });
+          }
+          const int64_t pick = order[std::min(next_far++, order.size() - 1)];
+          for (int j = 0; j < d; ++j) ck[j] = train[(size_t)pick * d + j];
+        }
+      }
+    }
+    for (size_t i = 0; i < C.size(); ++i) centroids[i] = (float)C[i];
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  ET_API_END
+}

@@ -39,6 +39,33 @@ __device__ __forceinline__ int tab_index(int lvl, int k, int i) {
   return ((lvl << 8) + k) * 32 + (i ^ (k & 31));
 }
 
+// Explicit shared-memory accesses (32-bit shared addresses; avoids generic
+// addressing in the hot loops).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float lds(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+// predicated load: v is returned unchanged when !pred (no shared-memory traffic)
+__device__ __forceinline__ float lds_if(uint32_t a, bool pred, float v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
+               : "+f"(v) : "r"(a), "r"((int)pred));
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" :: "r"(a), "f"(v) : "memory");
+}
+// byte address of table entry (level, k, lane): see tab_index
+__device__ __forceinline__ uint32_t tab_addr(uint32_t tab_s, int lvl, uint32_t k, uint32_t lane4) {
+  return tab_s + ((uint32_t)lvl << 15) + (k << 7) + ((lane4 ^ (k << 2)) & 0x7cu);
+}
+
 // Squared distance between the query sub-vector x[0..s) (optionally minus the
 // coarse centroid cc) and codeword c (registers), fp32, j ascending, FMA.
 template <int SS>
@@ -279,8 +306,10 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
   const int nb = (K + 31) >> 5;
   const int lane = lane_id(), warp = warp_id();
   float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
-  float* region = sm.tab + (size_t)(MT - 1 - lv0) * 256 * 32;   // last level's table region
-  // ---- stage: levels 0..MT-2 -> region [l][i][16]; level MT-1 -> sm.stage [i][16]
+  const uint32_t tab_s = smem_u32(sm.tab);
+  const uint32_t region_s = tab_s + ((uint32_t)(MT - 1 - lv0) << 15);   // last level's table region
+  const uint32_t stage_s = smem_u32(sm.stage);
+  // ---- stage: levels 0..MT-2 -> region [l][i][16]; level MT-1 -> stage [i][16]
   const int per_level = nq * SS;
   const int total = MT * per_level;
   __syncthreads();                                   // previous tree's scan is done with the tables
@@ -291,57 +320,81 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
     const int q = sm.qidx[i];
     float v = __ldg(p.queries + (size_t)q * d + (size_t)m * SS + j);
     if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * SS + j);
-    if (l < MT - 1) region[e] = v;
-    else sm.stage[r] = v;
+    if (l < MT - 1) sts(region_s + 4u * e, v);
+    else sts(stage_s + 4u * r, v);
   }
   __syncthreads();
   const int G = max(1, kWarps / nb);
-  auto item = [&](int l, int kb, int g, const float* xs, int xstride) {
+  const uint32_t lane4 = (uint32_t)lane << 2;
+  auto load_cw = [&](int l, int kb, float (&c)[SS]) {
     const int k = kb * 32 + lane;
     const bool kvalid = k < K;
     const int m = p.layer_sub[tr.layer0 + l];
     const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
-    float c[SS];
 #pragma unroll
     for (int j = 0; j < SS; j += 4) {
       const float4 v = kvalid ? __ldg(reinterpret_cast<const float4*>(crow + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
       c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
     }
+  };
+  auto item = [&](int l, int kb, int g, uint32_t xs_s, const float (&c)[SS]) {
+    const uint32_t k = (uint32_t)(kb * 32 + lane);
+    const bool kvalid = (int)k < K;
+    auto put = [&](int i, float a) {
+      if (!kvalid) return;
+      if (l < lv0) lut0[k * 32 + i] = a;
+      else sts(tab_addr(tab_s, l - lv0, k, (uint32_t)i << 2), a);
+    };
     int i = g;
     for (; i + G < nq; i += 2 * G) {
-      const float* x0 = xs + i * xstride;
-      const float* x1 = xs + (i + G) * xstride;
+      const uint32_t x0 = xs_s + (uint32_t)i * (SS * 4);
+      const uint32_t x1 = xs_s + (uint32_t)(i + G) * (SS * 4);
       float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-      for (int j = 0; j < SS; ++j) {
-        const float t0 = x0[j] - c[j];
-        const float t1 = x1[j] - c[j];
-        a0 = fmaf(t0, t0, a0);
-        a1 = fmaf(t1, t1, a1);
+      for (int j = 0; j < SS; j += 4) {
+        const float4 u0 = lds4(x0 + 4 * j), u1 = lds4(x1 + 4 * j);
+        float t0, t1;
+        t0 = u0.x - c[j];     t1 = u1.x - c[j];     a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
+        t0 = u0.y - c[j + 1]; t1 = u1.y - c[j + 1]; a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
+        t0 = u0.z - c[j + 2]; t1 = u1.z - c[j + 2]; a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
+        t0 = u0.w - c[j + 3]; t1 = u1.w - c[j + 3]; a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
       }
-      if (kvalid) {
-        *tab_slot(sm, lut0, l, lv0, k, i) = a0;
-        *tab_slot(sm, lut0, l, lv0, k, i + G) = a1;
-      }
+      put(i, a0);
+      put(i + G, a1);
     }
     if (i < nq) {
-      const float* x0 = xs + i * xstride;
+      const uint32_t x0 = xs_s + (uint32_t)i * (SS * 4);
       float a0 = 0.f;
 #pragma unroll
-      for (int j = 0; j < SS; ++j) {
-        const float t0 = x0[j] - c[j];
-        a0 = fmaf(t0, t0, a0);
+      for (int j = 0; j < SS; j += 4) {
+        const float4 u0 = lds4(x0 + 4 * j);
+        float t0;
+        t0 = u0.x - c[j];     a0 = fmaf(t0, t0, a0);
+        t0 = u0.y - c[j + 1]; a0 = fmaf(t0, t0, a0);
+        t0 = u0.z - c[j + 2]; a0 = fmaf(t0, t0, a0);
+        t0 = u0.w - c[j + 3]; a0 = fmaf(t0, t0, a0);
       }
-      if (kvalid) *tab_slot(sm, lut0, l, lv0, k, i) = a0;
+      put(i, a0);
     }
   };
   const int per = nb * G;
-  for (int it = warp; it < (MT - 1) * per; it += kWarps) {
+  const int n_items = (MT - 1) * per;
+  float cw[SS], cwn[SS];
+  int it = warp;
+  if (it < n_items) load_cw(it / per, (it % per) % nb, cw);
+  for (; it < n_items; it += kWarps) {
     const int l = it / per, r = it - l * per;
-    item(l, r % nb, r / nb, region + (size_t)l * per_level, SS);
+    const int nx = it + kWarps;
+    if (nx < n_items) load_cw(nx / per, (nx % per) % nb, cwn);   // prefetch the next item's codeword
+    item(l, r % nb, r / nb, region_s + ((uint32_t)l * per_level) * 4u, cw);
+#pragma unroll
+    for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
   }
   __syncthreads();                                   // region free: build the last level into it
-  for (int it = warp; it < per; it += kWarps) item(MT - 1, it % nb, it / nb, sm.stage, SS);
+  for (int it2 = warp; it2 < per; it2 += kWarps) {
+    load_cw(MT - 1, it2 % nb, cw);
+    item(MT - 1, it2 % nb, it2 / nb, stage_s, cw);
+  }
   __syncthreads();
 }
 
@@ -590,7 +643,8 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
   const ScanParams& p = *e.p;
   constexpr int lv0 = (MT == 8) ? 1 : 0;
   const int lane = lane_id();
-  const float* tab = sm.tab;
+  const uint32_t tab_s = smem_u32(sm.tab);
+  const uint32_t lane4 = (uint32_t)lane << 2;
   const uint32_t tq = tmem_lane_base(sm.tmem);
   float ctx[MT];
 #pragma unroll
@@ -613,13 +667,11 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
       if (base + j == a) pl = 0;   // first leaf of this warp's range: rebuild the whole path
       float v[MT];
       uint32_t v0t = 0;
+      if (lv0 > 0 && pl == 0) v0t = tmem_ld1(tq + (lo & 255u));   // level 0 from TMEM
 #pragma unroll
-      for (int l = 0; l < MT; ++l) {
-        if (l >= pl) {
-          const uint32_t kb = ((l < 4 ? lo : hi) >> (8 * (l & 3))) & 255u;
-          if (l < lv0) v0t = tmem_ld1(tq + kb);
-          else v[l] = tab[tab_index(l - lv0, kb, lane)];
-        }
+      for (int l = lv0; l < MT; ++l) {
+        const uint32_t kb = ((l < 4 ? lo : hi) >> (8 * (l & 3))) & 255u;
+        v[l] = lds_if(tab_addr(tab_s, l - lv0, kb, lane4), l >= pl, 0.f);
       }
       if (lv0 > 0 && pl == 0) {
         tmem_wait_ld(v0t);
@@ -864,6 +916,7 @@ struct FinSmem {
   uint32_t mul[kFinWarps][kFinCap];
   uint32_t hist[kFinWarps][256];
   unsigned long long stage[kFinWarps][kTopkMax];
+  unsigned long long xs[kFinWarps][kTopkMax];   // slow-path (distance, id) keys
   int nstage[kFinWarps];
   uint32_t tied_g[kFinWarps];
 };
@@ -1037,19 +1090,20 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   }
   const uint32_t t = all ? 0xffffffffu : prefix;
 
-  // 4. collect ids: all of every group < t, then the R smallest ids among tied groups
+  // 4. output.  Groups with distance < t contribute all their ids (< k in
+  //    total); among groups tied at t the R = k - mult(< t) smallest ids.
+  //    Fast path: sort only the (few) groups < t by distance; when no two of
+  //    them share a distance, each group's ids (ascending) are already in
+  //    (distance, id) order and are written out directly.
   unsigned long long* stage = fs.stage[warp];
   if (lane == 0) fs.nstage[warp] = 0;
   __syncwarp();
   uint32_t slt = 0, ntied = 0;
   src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
     if (key < t || all) {
-      const uint32_t o0 = __ldg(p.group_off + g);
       slt += mu;
-      const int pos = atomicAdd(&fs.nstage[warp], (int)mu);
-      for (uint32_t o = 0; o < mu; ++o)
-        if (pos + (int)o < kTopkMax)
-          stage[pos + o] = ((unsigned long long)key << 32) | (uint32_t)__ldg(p.ids + o0 + o);
+      const int pos = atomicAdd(&fs.nstage[warp], 1);
+      if (pos < kTopkMax) stage[pos] = ((unsigned long long)key << 32) | g;
     } else if (key == t) {
       ntied += 1;
       fs.tied_g[warp] = g;
@@ -1058,18 +1112,90 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   slt = __reduce_add_sync(FULLMASK, slt);
   ntied = __reduce_add_sync(FULLMASK, ntied);
   __syncwarp();
+  const int ng = min(fs.nstage[warp], kTopkMax);   // groups < t (< k of them)
+  {
+    int np2 = 32;
+    while (np2 < ng) np2 <<= 1;
+    for (int i = ng + lane; i < np2; i += 32) stage[i] = ~0ull;
+    __syncwarp();
+    if (ng > 1) warp_bitonic_sort(stage, np2);
+  }
+  // exact distance ties between different groups < t need an id merge (slow path)
+  bool dup = false;
+  for (int i = lane; i + 1 < ng; i += 32) dup |= (stage[i] >> 32) == (stage[i + 1] >> 32);
+  dup = __any_sync(FULLMASK, dup);
+  float* od = p.out_dist + (size_t)q * k;
+  int32_t* oi = p.out_ids + (size_t)q * k;
+  int written = 0;
+  if (!dup) {
+    // prefix offsets of the sorted groups' multiplicities, 32 groups at a time
+    for (int g0 = 0; g0 < ng; g0 += 32) {
+      const int gi = g0 + lane;
+      uint32_t key = 0, g = 0, mu = 0, o0 = 0;
+      if (gi < ng) {
+        key = (uint32_t)(stage[gi] >> 32);
+        g = (uint32_t)(stage[gi] & 0xffffffffu);
+        o0 = __ldg(p.group_off + g);
+        mu = __ldg(p.group_off + g + 1) - o0;
+      }
+      uint32_t inc = mu;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULLMASK, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const uint32_t base = (uint32_t)written + inc - mu;
+      const int cnt = min(32, ng - g0);
+      for (int j = 0; j < cnt; ++j) {   // lanes copy group j's ids
+        const uint32_t bj = __shfl_sync(FULLMASK, base, j);
+        const uint32_t mj = __shfl_sync(FULLMASK, mu, j);
+        const uint32_t oj = __shfl_sync(FULLMASK, o0, j);
+        const float dj = __uint_as_float(__shfl_sync(FULLMASK, key, j));
+        for (uint32_t r = lane; r < mj; r += 32)
+          if (bj + r < (uint32_t)k) { od[bj + r] = dj; oi[bj + r] = __ldg(p.ids + oj + r); }
+      }
+      written += (int)__shfl_sync(FULLMASK, inc, 31);
+    }
+  } else {
+    // slow path: expand every group < t into (distance, id) keys and sort them
+    __syncwarp();
+    int n_ids = 0;
+    for (int gi = 0; gi < ng; ++gi) {
+      const uint32_t key = (uint32_t)(stage[gi] >> 32), g = (uint32_t)(stage[gi] & 0xffffffffu);
+      const uint32_t o0 = __ldg(p.group_off + g), mu = __ldg(p.group_off + g + 1) - o0;
+      unsigned long long* xs = fs.xs[warp];
+      for (uint32_t r = lane; r < mu; r += 32)
+        if (n_ids + (int)r < kTopkMax)
+          xs[n_ids + r] = ((unsigned long long)key << 32) | (uint32_t)__ldg(p.ids + o0 + r);
+      n_ids += (int)mu;
+    }
+    __syncwarp();
+    n_ids = min(n_ids, kTopkMax);
+    int np2 = 32;
+    while (np2 < n_ids) np2 <<= 1;
+    unsigned long long* xs = fs.xs[warp];
+    for (int i = n_ids + lane; i < np2; i += 32) xs[i] = ~0ull;
+    __syncwarp();
+    warp_bitonic_sort(xs, np2);
+    for (int i = lane; i < n_ids && i < k; i += 32) {
+      od[i] = __uint_as_float((uint32_t)(xs[i] >> 32));
+      oi[i] = (int32_t)(uint32_t)(xs[i] & 0xffffffffu);
+    }
+    written = n_ids;
+  }
+  written = min(written, k);
+  __syncwarp();
   if (!all && ntied == 1) {
     // common case: one group holds the k-th distance -> its R smallest ids
     const uint32_t R = (uint32_t)k - slt;
     const uint32_t g = fs.tied_g[warp];
     const uint32_t o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
     const uint32_t take = min(R, o1 - o0);
-    const int base = fs.nstage[warp];
-    for (uint32_t i = lane; i < take; i += 32)
-      if (base + (int)i < kTopkMax)
-        stage[base + i] = ((unsigned long long)t << 32) | (uint32_t)__ldg(p.ids + o0 + i);
-    __syncwarp();
-    if (lane == 0) fs.nstage[warp] = base + (int)take;
+    for (uint32_t i = lane; i < take; i += 32) {
+      od[written + i] = __uint_as_float(t);
+      oi[written + i] = __ldg(p.ids + o0 + i);
+    }
+    written += (int)take;
   } else if (!all && ntied > 1) {
     const uint32_t R = (uint32_t)k - slt;
     // tau: R-th smallest minid among tied groups (only groups with minid <= tau matter)
@@ -1111,6 +1237,8 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
       }
       sigma = w;
     }
+    if (lane == 0) fs.nstage[warp] = 0;
+    __syncwarp();
     src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
       if (key != t || (uint32_t)__ldg(p.group_minid + g) > tau) return;
       const uint32_t o0 = __ldg(p.group_off + g);
@@ -1118,27 +1246,26 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
         const uint32_t id = (uint32_t)__ldg(p.ids + o0 + o);
         if (id > sigma) break;
         const int pos = atomicAdd(&fs.nstage[warp], 1);
-        if (pos < kTopkMax) stage[pos] = ((unsigned long long)key << 32) | id;
+        if (pos < kTopkMax) stage[pos] = id;
       }
     });
-  }
-  __syncwarp();
-  int ns = min(fs.nstage[warp], kTopkMax);
-  int np2 = 32;
-  while (np2 < ns) np2 <<= 1;
-  for (int i = ns + lane; i < np2; i += 32) stage[i] = ~0ull;
-  __syncwarp();
-  warp_bitonic_sort(stage, np2);
-  for (int i = lane; i < k; i += 32) {
-    float dv = __int_as_float(0x7f800000);
-    int32_t iv = -1;
-    if (i < ns) {
-      const unsigned long long v = stage[i];
-      dv = __uint_as_float((uint32_t)(v >> 32));
-      iv = (int32_t)(uint32_t)(v & 0xffffffffu);
+    __syncwarp();
+    const int nt = min(fs.nstage[warp], (int)R);
+    int np2 = 32;
+    while (np2 < fs.nstage[warp] && np2 < kTopkMax) np2 <<= 1;
+    for (int i = fs.nstage[warp] + lane; i < np2; i += 32) stage[i] = ~0ull;
+    __syncwarp();
+    warp_bitonic_sort(stage, np2);
+    for (int i = lane; i < nt && written + i < k; i += 32) {
+      od[written + i] = __uint_as_float(t);
+      oi[written + i] = (int32_t)(uint32_t)stage[i];
     }
-    p.out_dist[(size_t)q * k + i] = dv;
-    p.out_ids[(size_t)q * k + i] = iv;
+    written += nt;
+  }
+  written = min(written, k);
+  for (int i = written + lane; i < k; i += 32) {
+    od[i] = __int_as_float(0x7f800000);
+    oi[i] = -1;
   }
 }
 
