@@ -297,19 +297,47 @@ def run_ours(args):
     st = prepare_ours(cfg, dev, rank, world)
     ix, qd, cbd = st["ix"], st["q_dev"], st["cb_dev"]
     stats = ix.stats()
-    dist_out = torch.empty((Q, k), dtype=torch.float32, device=dev)
-    ids_out = torch.empty((Q, k), dtype=torch.int32, device=dev)
+    kk = max(k, 1)
+    dist_out = torch.empty((Q, kk), dtype=torch.float32, device=dev)
+    ids_out = torch.empty((Q, kk), dtype=torch.int32, device=dev)
     if world > 1:
-        gd = torch.empty((world, Q, k), dtype=torch.float32, device=dev)
-        gi = torch.empty((world, Q, k), dtype=torch.int32, device=dev)
+        gd = torch.empty((world, Q, kk), dtype=torch.float32, device=dev)
+        gi = torch.empty((world, Q, kk), dtype=torch.int32, device=dev)
+
+    full = (k == 0)
+    ivf = bool(cfg.ivf_nlist)
+    if full:
+        full_out = torch.empty((Q, ix.N), dtype=torch.float32, device=dev)
+
+    def local_step(q_in):
+        if full:
+            return ix.et_etree_distances(queries=q_in, codebooks=cbd, out=full_out)
+        if ivf:
+            d_, i_ = ix.et_ivf_topk(q_in, nprobe=cfg.ivf_nprobe, k=k)
+            dist_out.copy_(d_)
+            ids_out.copy_(i_)
+            return dist_out, ids_out
+        return ix.et_etree_topk(k, queries=q_in, codebooks=cbd, out=(dist_out, ids_out))
 
     def step():
-        ix.et_etree_topk(k, queries=qd, codebooks=cbd, out=(dist_out, ids_out))
-        if world > 1:
+        r = local_step(qd)
+        if world > 1 and not full:
             dist.all_gather_into_tensor(gd, dist_out)
             dist.all_gather_into_tensor(gi, ids_out)
             return api.et_merge_topk(gd, gi)
-        return dist_out, ids_out
+        return r
+
+    # query.code pairs per step (IVF: sum of the probed lists' sizes)
+    if ivf:
+        _, _, pr = ix.et_ivf_topk(qd, nprobe=cfg.ivf_nprobe, k=k, return_probes=True)
+        pairs = int(st["list_sizes"][pr.cpu().numpy().ravel()].sum())
+        if world > 1:
+            t = torch.tensor([pairs], device=dev, dtype=torch.float64)
+            dist.all_reduce(t)
+            pairs = int(t.item())
+    else:
+        pairs = Q * cfg.N
+    k_alloc = max(k, 1)
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     for _ in range(max(3, args.warmup)):
@@ -352,7 +380,7 @@ def run_ours(args):
         t = torch.tensor([step_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         step_ms = float(t.item())
-    value = Q * cfg.N / (step_ms / 1e3)
+    value = pairs / (step_ms / 1e3)
 
     # per-kernel breakdown: the same steps, library events around each launch
     api.et_timing_reset()
@@ -362,7 +390,7 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     kern = {}
-    for name in ("fill", "scan", "finalize", "luts", "gather"):
+    for name in ("fill", "probe", "bucket", "scan", "finalize", "luts", "gather"):
         ms, n = api.et_timing_get(name)
         if n:
             kern[name] = ms / n
@@ -371,8 +399,9 @@ def run_ours(args):
 
     # e2e: host (pinned) queries in, top-k out, copies inside the timed region
     qh = torch.from_numpy(st["qx"]).pin_memory()
-    dh = torch.empty((Q, k), dtype=torch.float32).pin_memory()
-    ih = torch.empty((Q, k), dtype=torch.int32).pin_memory()
+    out_shape = (Q, cfg.N) if full else (Q, kk)
+    dh = torch.empty(out_shape, dtype=torch.float32).pin_memory()
+    ih = torch.empty((Q, kk), dtype=torch.int32).pin_memory()
     q_stage = torch.empty_like(qd)
     e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
              for _ in range(max(5, args.steps // 4))]
@@ -381,15 +410,18 @@ def run_ours(args):
         flush.fill_(1.0)
         a.record()
         q_stage.copy_(qh, non_blocking=True)
-        ix.et_etree_topk(k, queries=q_stage, codebooks=cbd, out=(dist_out, ids_out))
-        if world > 1:
-            dist.all_gather_into_tensor(gd, dist_out)
-            dist.all_gather_into_tensor(gi, ids_out)
-            md, mi = api.et_merge_topk(gd, gi)
+        r = local_step(q_stage)
+        if full:
+            dh.copy_(r, non_blocking=True)
         else:
-            md, mi = dist_out, ids_out
-        dh.copy_(md, non_blocking=True)
-        ih.copy_(mi, non_blocking=True)
+            if world > 1:
+                dist.all_gather_into_tensor(gd, dist_out)
+                dist.all_gather_into_tensor(gi, ids_out)
+                md, mi = api.et_merge_topk(gd, gi)
+            else:
+                md, mi = dist_out, ids_out
+            dh.copy_(md, non_blocking=True)
+            ih.copy_(mi, non_blocking=True)
         b.record()
     torch.cuda.synchronize()
     e2e_ms = sum(a.elapsed_time(b) for a, b in e_evs) / len(e_evs)
@@ -400,9 +432,24 @@ def run_ours(args):
 
     peaks, peak_src = load_peaks()
     if rank == 0:
-        roof = roofline(cfg, stats, kern["scan"], peaks, clk.summary()["sm_mhz"], Q)
+        if full and kern.get("gather", 0) > kern.get("scan", 0):
+            hbm = float(peaks.get("hbm_gbs", 6558.1))
+            byts = Q * cfg.N * 4 + cfg.N * 4
+            ach = byts / (kern["gather"] / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(ach / hbm, 4), "traffic": None,
+                    "kernel": "gather_full_kernel (Q x N fp32 output write)",
+                    "note": "algorithmic bytes = 4*Q*N output + 4*N slot->leaf map"}
+            dom_ms = kern["gather"]
+        else:
+            n_tables = Q * cfg.ivf_nprobe if ivf else Q
+            lookups = None
+            if ivf:
+                lookups = stats[0]["lookups"] / max(1, cfg.N) * pairs
+            roof = roofline(cfg, stats, kern["scan"], peaks, clk.summary()["sm_mhz"], Q, n_tables, lookups)
+            dom_ms = kern["scan"]
         roof["peak_source"] = peak_src
-        roof["share_of_step"] = round(kern["scan"] / sum(kern.values()), 4)
+        roof["share_of_step"] = round(dom_ms / sum(kern.values()), 4)
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
             with open(tr) as f:
@@ -412,7 +459,9 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: BASELINE configs[{['c1','c2','c3','c4','c5'].index(cfg.name) if cfg.name in ['c1','c2','c3','c4','c5'] else 'diag'}]",
+            "config": {"workload": (f"{cfg.name}: BASELINE configs[{['c1','c2','c3','c4','c5'].index(cfg.name)}]"
+                                    if cfg.name in ['c1', 'c2', 'c3', 'c4', 'c5'] else f"{cfg.name}: diagnostic companion"),
+                       "pairs_per_step": pairs,
                        "N": cfg.N, "d": cfg.d, "M": cfg.M, "K": cfg.K, "Q": Q, "k": k,
                        "forest_split": cfg.forest_split,
                        "parallelism": f"db-shard{world} (first-level subtrees) + all-gather" if world > 1 else "1 GPU",
@@ -422,14 +471,15 @@ def run_ours(args):
             "north_star_roofline": north_star_roofline(cfg, stats, step_ms, peaks, Q),
             "kernels_ms": {k_: round(v, 5) for k_, v in kern.items()},
             "dominant_kernel": dom,
-            "e2e": {"value": Q * cfg.N / (e2e_ms / 1e3), "unit": UNIT,
-                    "h2d_bytes_per_step": int(qh.numel() * 4), "d2h_bytes_per_step": int(Q * k * 8),
+            "e2e": {"value": pairs / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(qh.numel() * 4),
+                    "d2h_bytes_per_step": int(dh.numel() * 4 + (0 if full else ih.numel() * 4)),
                     "ms_per_step": e2e_ms},
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk.summary(),
             "tree_stats": [{kk: s[kk] for kk in ("L1", "L2", "total_postfix", "lookups", "paper_bytes")} for s in stats],
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not ivf:
             out["cpu_baseline"] = cpu_baseline(cfg, st["cb"], st["codes"], st["qx"])
         print(json.dumps(out), flush=True)
     if world > 1:

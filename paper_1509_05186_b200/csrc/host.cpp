@@ -224,7 +224,7 @@ static void tree_stats(HostTree& t, int64_t N) {
   t.st.lookups = look;
   t.st.L2_records = recs;
   t.st.paper_bytes = 4 * N + 2 * (L1 + recs) + post_recs;
-  t.st.device_bytes = L2 * 9;
+  t.st.device_bytes = L2 * 17;
 }
 
 static void check_codes(const uint8_t* codes, int64_t n, int M, int K) {
@@ -276,9 +276,28 @@ static void upload_groups(et_index* ix, const Groups& g, const std::vector<uint3
   if (!slot2group.empty()) ix->slot2group.upload(slot2group);
 }
 
+// Leaf records of the device layout: for each level l the
+// pre-swizzled byte offset of table entry (l, k = code byte l) inside that
+// level's 32 KB shared-memory table, (k << 7) | ((k & 31) << 2), so a lookup is
+// one XOR with the lane's offset; level 0 of an 8-level tree (held in TMEM)
+// stores the raw column k.
+static std::vector<uint4> make_records(const std::vector<uint64_t>& code, int MT) {
+  std::vector<uint4> rec(code.size());
+  for (size_t i = 0; i < code.size(); ++i) {
+    uint16_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int l = 0; l < MT; ++l) {
+      const uint32_t k = (uint32_t)((code[i] >> (8 * l)) & 255u);
+      w[l] = (MT == 8 && l == 0) ? (uint16_t)k : (uint16_t)((k << 7) | ((k & 31u) << 2));
+    }
+    rec[i] = make_uint4(w[0] | ((uint32_t)w[1] << 16), w[2] | ((uint32_t)w[3] << 16),
+                        w[4] | ((uint32_t)w[5] << 16), w[6] | ((uint32_t)w[7] << 16));
+  }
+  return rec;
+}
+
 static void finish_tree(et_index* ix, int t, HostTree& h) {
   ix->n_leaves[t] = (int64_t)h.code.size();
-  ix->code[t].upload(h.code);
+  ix->code[t].upload(make_records(h.code, h.MT));
   ix->lcp[t].upload(h.lcp);
   ix->stats[t] = h.st;
 }
@@ -416,7 +435,7 @@ static et_index* build_flat(const uint8_t* codes, const int32_t* ids, int64_t n,
   h.lcp.assign(n, 0);
   h.mult.assign(n, 1);
   for (int64_t i = 0; i < n; ++i) h.code[i] = pack(codes + (size_t)i * M, 0, M);
-  h.st.N = n; h.st.M = M; h.st.L2 = n; h.st.lookups = n * M; h.st.device_bytes = n * 9;
+  h.st.N = n; h.st.M = M; h.st.L2 = n; h.st.lookups = n * M; h.st.device_bytes = n * 17;
   h.st.L2_records = n; h.st.total_postfix = n * (M - 1); h.st.paper_bytes = 4 * n + n * M;
   finish_tree(ix.get(), 0, h);
   Groups g;
@@ -490,10 +509,10 @@ static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t 
     for (size_t j = 0; j + 1 < g.off.size(); ++j) std::sort(g.ids.begin() + g.off[j], g.ids.begin() + g.off[j + 1]);
   }
   upload_groups(ix.get(), g, s2g);
-  tot.N = n; tot.M = M; tot.device_bytes = (int64_t)h.code.size() * 9;
+  tot.N = n; tot.M = M; tot.device_bytes = (int64_t)h.code.size() * 17;
   tot.groups = (int64_t)(g.off.size() - 1);
   ix->n_leaves[0] = (int64_t)h.code.size();
-  ix->code[0].upload(h.code);
+  ix->code[0].upload(make_records(h.code, M));
   ix->lcp[0].upload(h.lcp);
   ix->stats[0] = tot;
   ix->list_leaf_off_d.upload(ix->list_leaf_off);
@@ -653,7 +672,7 @@ static void fill_scan_common(ScanParams& sp, const et_index* ix, const Plan& pl)
     sp.tree[t].MT = ix->stats[t].M;
     sp.tree[t].layer0 = ix->split[t];
     sp.tree[t].n_leaves = ix->n_leaves[t];
-    sp.tree[t].code = ix->code[t].as<uint64_t>();
+    sp.tree[t].rec = ix->code[t].as<uint4>();
     sp.tree[t].lcp = ix->lcp[t].as<uint8_t>();
     sp.tup_leaf[t] = ix->tup_leaf[t].as<uint32_t>();
     sp.part_base[t] = pl.part_base[t];

@@ -20,12 +20,15 @@ constexpr int kFinWarps = 8;               // warps per finalize CTA
 // the length of its common prefix with the previous leaf.  The internal nodes
 // of the paper's Hierarchical Memory Structure are implicit: a leaf whose LCP
 // with its predecessor is p enters the new internal nodes at depths p..depth-1,
-// whose K fields are the leaf's own code bytes.
+// whose K fields are the leaf's own code bytes.  The code is stored
+// "compiled": 16 bits per level = the pre-swizzled shared-memory byte offset of
+// table entry (l, code byte l) -- (k << 7) | ((k & 31) << 2) -- or, for level 0
+// of an 8-level tree (TMEM), the raw byte k.
 struct TreeDev {
   int MT = 0;                  // levels of this tree
   int layer0 = 0;              // first code byte it covers
   int64_t n_leaves = 0;
-  const uint64_t* code = nullptr;   // byte l of the code at bits 8l..8l+7
+  const uint4* rec = nullptr;       // 8 x u16 per leaf (level l in half-word l)
   const uint8_t* lcp = nullptr;     // LCP with the previous leaf (0 for leaf 0)
 };
 

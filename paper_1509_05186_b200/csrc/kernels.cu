@@ -58,6 +58,13 @@ __device__ __forceinline__ float lds_if(uint32_t a, bool pred, float v) {
                : "+f"(v) : "r"(a), "r"((int)pred));
   return v;
 }
+// predicated load; the result is undefined when !pred (callers never use it then)
+__device__ __forceinline__ float lds_if_w(uint32_t a, bool pred) {
+  float v;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
+               : "=f"(v) : "r"(a), "r"((int)pred));
+  return v;
+}
 __device__ __forceinline__ void sts(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" :: "r"(a), "f"(v) : "memory");
 }
@@ -654,24 +661,27 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
   for (uint32_t base = a; base < b; base += 32, ++batch) {
     const uint32_t idx = base + lane;
     const bool in = idx < b;
-    const uint64_t mycode = in ? __ldg(tr.code + idx) : 0ull;
+    const uint4 myrec = in ? __ldg(tr.rec + idx) : make_uint4(0u, 0u, 0u, 0u);
     const uint32_t mylcp = in ? (uint32_t)__ldg(tr.lcp + idx) : 0u;
     uint32_t aux0 = 0, aux1 = 0;   // role 1: multiplicity; role 2: tuple range
     if (ROLE == 1 && topk && in) aux0 = __ldg(p.group_mult + idx);
     if (ROLE == 2 && in) { aux0 = __ldg(p.t0_tup_off + idx); aux1 = __ldg(p.t0_tup_off + idx + 1); }
     const int n = (int)min(32u, b - base);
     for (int j = 0; j < n; ++j) {
-      const uint32_t lo = __shfl_sync(FULLMASK, (uint32_t)mycode, j);
-      const uint32_t hi = __shfl_sync(FULLMASK, (uint32_t)(mycode >> 32), j);
+      uint32_t w4[4];
+      w4[0] = __shfl_sync(FULLMASK, myrec.x, j);
+      w4[1] = (MT > 2) ? __shfl_sync(FULLMASK, myrec.y, j) : 0u;
+      w4[2] = (MT > 4) ? __shfl_sync(FULLMASK, myrec.z, j) : 0u;
+      w4[3] = (MT > 6) ? __shfl_sync(FULLMASK, myrec.w, j) : 0u;
       int pl = (int)__shfl_sync(FULLMASK, mylcp, j);
       if (base + j == a) pl = 0;   // first leaf of this warp's range: rebuild the whole path
       float v[MT];
       uint32_t v0t = 0;
-      if (lv0 > 0 && pl == 0) v0t = tmem_ld1(tq + (lo & 255u));   // level 0 from TMEM
+      if (lv0 > 0 && pl == 0) v0t = tmem_ld1(tq + (w4[0] & 0xffffu));   // level 0 from TMEM
 #pragma unroll
       for (int l = lv0; l < MT; ++l) {
-        const uint32_t kb = ((l < 4 ? lo : hi) >> (8 * (l & 3))) & 255u;
-        v[l] = lds_if(tab_addr(tab_s, l - lv0, kb, lane4), l >= pl, 0.f);
+        const uint32_t w = (l & 1) ? (w4[l >> 1] >> 16) : (w4[l >> 1] & 0xffffu);
+        v[l] = lds_if_w(tab_s + (w ^ lane4) + ((uint32_t)(l - lv0) << 15), l >= pl);
       }
       if (lv0 > 0 && pl == 0) {
         tmem_wait_ld(v0t);
