@@ -39,6 +39,13 @@ __device__ __forceinline__ int tab_index(int lvl, int k, int i) {
   return ((lvl << 8) + k) * 32 + (i ^ (k & 31));
 }
 
+// Dynamic shared memory of the scan kernel, addressed by byte offset through
+// this extern array so the compiler emits LDS/STS (and may reorder loads).
+extern __shared__ __align__(16) unsigned char et_dsm[];
+__device__ __forceinline__ float4 lds4_off(uint32_t off) {
+  return *reinterpret_cast<const float4*>(et_dsm + off);
+}
+
 // Explicit shared-memory accesses (32-bit shared addresses; avoids generic
 // addressing in the hot loops).
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -302,12 +309,11 @@ __device__ __forceinline__ void build_pass_generic(const SmemScan& sm, float* lu
 // shared-memory region of the tree's LAST level (not built yet), those levels
 // are built without barriers, then the last level is built from the small
 // stage.  Three barriers per tree instead of two per pass.
-template <int SS>
+template <int SS, int MT>
 __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq,
                                       int cell) {
   static_assert(SS == kDC, "resident staging handles s == 16");
   const TreeDev& tr = p.tree[t];
-  const int MT = tr.MT;
   const int lv0 = (MT == 8) ? 1 : 0;
   const int K = p.K, d = p.d;
   const int nb = (K + 31) >> 5;
@@ -316,19 +322,29 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
   const uint32_t tab_s = smem_u32(sm.tab);
   const uint32_t region_s = tab_s + ((uint32_t)(MT - 1 - lv0) << 15);   // last level's table region
   const uint32_t stage_s = smem_u32(sm.stage);
+  const uint32_t dsm_s = smem_u32(et_dsm);                               // offsets for lds4_off
   // ---- stage: levels 0..MT-2 -> region [l][i][16]; level MT-1 -> stage [i][16]
   const int per_level = nq * SS;
-  const int total = MT * per_level;
   __syncthreads();                                   // previous tree's scan is done with the tables
-  for (int e = threadIdx.x; e < total; e += kThreads) {
-    const int l = e / per_level, r = e - l * per_level;
-    const int i = r / SS, j = r - i * SS;
-    const int m = p.layer_sub[tr.layer0 + l];
-    const int q = sm.qidx[i];
-    float v = __ldg(p.queries + (size_t)q * d + (size_t)m * SS + j);
-    if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * SS + j);
-    if (l < MT - 1) sts(region_s + 4u * e, v);
-    else sts(stage_s + 4u * r, v);
+  {
+    // thread t stages dimension j = t % 16 of query slot i = t / 16 for every
+    // level: all loads first (independent), then the stores
+    const int i = threadIdx.x >> 4, j = threadIdx.x & (SS - 1);
+    if (i < nq) {
+      const int q = sm.qidx[i];
+      const float* xr = p.queries + (size_t)q * d + j;
+      const float* cr = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + j : nullptr;
+      float v[MT];
+#pragma unroll
+      for (int l = 0; l < MT; ++l) v[l] = __ldg(xr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
+      if (cr) {
+#pragma unroll
+        for (int l = 0; l < MT; ++l) v[l] -= __ldg(cr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
+      }
+#pragma unroll
+      for (int l = 0; l < MT - 1; ++l) sts(region_s + 4u * (uint32_t)(l * per_level + i * SS + j), v[l]);
+      sts(stage_s + 4u * (uint32_t)(i * SS + j), v[MT - 1]);
+    }
   }
   __syncthreads();
   const int G = max(1, kWarps / nb);
@@ -354,12 +370,12 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
     };
     int i = g;
     for (; i + G < nq; i += 2 * G) {
-      const uint32_t x0 = xs_s + (uint32_t)i * (SS * 4);
-      const uint32_t x1 = xs_s + (uint32_t)(i + G) * (SS * 4);
+      const uint32_t x0 = xs_s - dsm_s + (uint32_t)i * (SS * 4);
+      const uint32_t x1 = xs_s - dsm_s + (uint32_t)(i + G) * (SS * 4);
       float a0 = 0.f, a1 = 0.f;
 #pragma unroll
       for (int j = 0; j < SS; j += 4) {
-        const float4 u0 = lds4(x0 + 4 * j), u1 = lds4(x1 + 4 * j);
+        const float4 u0 = lds4_off(x0 + 4 * j), u1 = lds4_off(x1 + 4 * j);
         float t0, t1;
         t0 = u0.x - c[j];     t1 = u1.x - c[j];     a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
         t0 = u0.y - c[j + 1]; t1 = u1.y - c[j + 1]; a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
@@ -370,11 +386,11 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
       put(i + G, a1);
     }
     if (i < nq) {
-      const uint32_t x0 = xs_s + (uint32_t)i * (SS * 4);
+      const uint32_t x0 = xs_s - dsm_s + (uint32_t)i * (SS * 4);
       float a0 = 0.f;
 #pragma unroll
       for (int j = 0; j < SS; j += 4) {
-        const float4 u0 = lds4(x0 + 4 * j);
+        const float4 u0 = lds4_off(x0 + 4 * j);
         float t0;
         t0 = u0.x - c[j];     a0 = fmaf(t0, t0, a0);
         t0 = u0.y - c[j + 1]; a0 = fmaf(t0, t0, a0);
@@ -603,7 +619,7 @@ struct EmitCtx {
 __device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, uint32_t mult) {
   const ScanParams& p = *e.p;
   if (p.mode == kModeFull) {
-    p.leafdist[((size_t)e.chunk * p.n_groups + g) * 32 + lane_id()] = dist;
+    p.leafdist[((size_t)e.chunk * 32 + lane_id()) * p.n_groups + g] = dist;   // query-major rows
     return;
   }
   TopkState& ts = e.ts;
@@ -675,21 +691,29 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
       w4[3] = (MT > 6) ? __shfl_sync(FULLMASK, myrec.w, j) : 0u;
       int pl = (int)__shfl_sync(FULLMASK, mylcp, j);
       if (base + j == a) pl = 0;   // first leaf of this warp's range: rebuild the whole path
-      float v[MT];
+      // Distance Context update, branch-free: s_l = (l >= p) ? s_{l-1} + T[l][k_l]
+      // : ctx[l] (ctx[l] of the shared prefix), ctx[l] = s_l.  The addition for
+      // l >= p is exactly ctx[l-1] + T[l][k_l] of P:249; for l < p the select
+      // keeps the prefix's value and the (unused) sum is discarded.
       uint32_t v0t = 0;
       if (lv0 > 0 && pl == 0) v0t = tmem_ld1(tq + (w4[0] & 0xffffu));   // level 0 from TMEM
+      float v[MT];
 #pragma unroll
       for (int l = lv0; l < MT; ++l) {
         const uint32_t w = (l & 1) ? (w4[l >> 1] >> 16) : (w4[l >> 1] & 0xffffu);
         v[l] = lds_if_w(tab_s + (w ^ lane4) + ((uint32_t)(l - lv0) << 15), l >= pl);
       }
-      if (lv0 > 0 && pl == 0) {
-        tmem_wait_ld(v0t);
+      if (lv0 > 0) {
+        if (pl == 0) tmem_wait_ld(v0t);
         v[0] = __uint_as_float(v0t);
       }
+      float sacc = 0.f;
 #pragma unroll
-      for (int l = 0; l < MT; ++l)
-        if (l >= pl) ctx[l] = (l == 0) ? v[0] : ctx[l > 0 ? l - 1 : 0] + v[l];
+      for (int l = 0; l < MT; ++l) {
+        const float t = sacc + v[l];
+        sacc = (l >= pl) ? t : ctx[l];
+        ctx[l] = sacc;
+      }
       const float dist = ctx[MT - 1];
       const uint32_t leaf = base + j;
       if constexpr (ROLE == 0) {
@@ -812,9 +836,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   // then tree 0, whose leaves walk their tuples and sum in tree order.
   for (int t = p.T - 1; t >= 0; --t) {
     const TreeDev& tr = p.tree[t];
-    if constexpr (SS == kDC) {
+    if constexpr (SS == kDC && MTC > 0) {
       if (p.luts) { build_tables<SS>(p, sm, t, unit, nq, cell); __syncthreads(); }
-      else build_tables_resident<SS>(p, sm, t, unit, nq, cell);
+      else build_tables_resident<SS, MTC>(p, sm, t, unit, nq, cell);
     } else {
       build_tables<SS>(p, sm, t, unit, nq, cell);
       __syncthreads();
@@ -1293,23 +1317,36 @@ cudaError_t launch_finalize(const FinParams& p, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // full output gather: out[q][slot] = leafdist[chunk(q)][group(slot)][lane(q)]
 // ---------------------------------------------------------------------------
-__global__ void gather_full_kernel(const float* __restrict__ leafdist, const uint32_t* __restrict__ slot2group,
-                                   int64_t n_groups, int64_t n, const int* __restrict__ qslot,
-                                   float* __restrict__ out, int use_smem) {
+__global__ void __launch_bounds__(1024) gather_full_kernel(const float* __restrict__ leafdist,
+                                                           const uint32_t* __restrict__ slot2group, int64_t n_groups,
+                                                           int64_t n, const int* __restrict__ qslot,
+                                                           float* __restrict__ out, int use_smem) {
   extern __shared__ float col[];
   const int64_t q = blockIdx.y;
   const int slot = qslot[q];
-  const int chunk = slot >> 5, ln = slot & 31;
-  const float* src = leafdist + (size_t)chunk * n_groups * 32 + ln;
+  const float* src = leafdist + (size_t)slot * n_groups;   // row of (chunk, lane) = slot
   if (use_smem) {
-    for (int64_t g = threadIdx.x; g < n_groups; g += blockDim.x) col[g] = __ldg(src + g * 32);
+    for (int64_t g = threadIdx.x; g < n_groups; g += blockDim.x) col[g] = __ldg(src + g);
     __syncthreads();
   }
   float* o = out + (size_t)q * n;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t g = __ldg(slot2group + i);
-    o[i] = use_smem ? col[g] : __ldg(src + (size_t)g * 32);
+  const int64_t per = (((n + gridDim.x - 1) / gridDim.x) + 3) & ~(int64_t)3;
+  const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n, i0 + per);
+  if ((n & 3) == 0 && (per & 3) == 0) {   // 16-byte stores
+    for (int64_t i = i0 + 4 * threadIdx.x; i < i1; i += 4 * blockDim.x) {
+      const uint4 g4 = __ldg(reinterpret_cast<const uint4*>(slot2group + i));
+      float4 v;
+      v.x = use_smem ? col[g4.x] : __ldg(src + g4.x);
+      v.y = use_smem ? col[g4.y] : __ldg(src + g4.y);
+      v.z = use_smem ? col[g4.z] : __ldg(src + g4.z);
+      v.w = use_smem ? col[g4.w] : __ldg(src + g4.w);
+      __stcs(reinterpret_cast<float4*>(o + i), v);
+    }
+  } else {
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      const uint32_t g = __ldg(slot2group + i);
+      o[i] = use_smem ? col[g] : __ldg(src + g);
+    }
   }
 }
 
@@ -1322,9 +1359,10 @@ cudaError_t launch_gather_full(const float* leafdist, const uint32_t* slot2group
     cudaError_t e = cudaFuncSetAttribute(gather_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  int bx = (int)std::min<int64_t>((n + 1023) / 1024, 64);
+  // ~2 CTAs per SM in total, each query's row split into bx slices
+  int64_t bx = std::max<int64_t>(1, std::min<int64_t>((296 + Q - 1) / Q, (n + 4095) / 4096));
   for (int64_t q0 = 0; q0 < Q; q0 += 65535) {
-    dim3 grid(bx, (unsigned)std::min<int64_t>(65535, Q - q0));
+    dim3 grid((unsigned)bx, (unsigned)std::min<int64_t>(65535, Q - q0));
     gather_full_kernel<<<grid, 1024, use_smem ? smem : 0, st>>>(leafdist, slot2group, n_groups, n, qslot + q0,
                                                                  out + (size_t)q0 * n, use_smem);
     count_launch();
