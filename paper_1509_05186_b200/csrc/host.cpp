@@ -915,7 +915,6 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   sp.cand = w.cand;
   sp.cand_cnt = w.cand_cnt;
   sp.unit_thr = w.unit_thr;
-  cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
   fp.flat_nchunks = pl.n_chunks;
@@ -926,7 +925,14 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   fp.group_minid = ix->group_minid.as<int32_t>();
   fp.unit_thr = w.unit_thr;
   fp.out_dist = dist; fp.out_ids = ids;
-  cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
+  if (pl.S == 1) {   // every query lives in one CTA: finalize inside the scan kernel
+    sp.fuse_fin = 1;
+    sp.fin = fp;
+    cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
+  } else {
+    cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
+    cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
+  }
   ET_API_END
 }
 

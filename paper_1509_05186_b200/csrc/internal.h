@@ -32,6 +32,24 @@ struct TreeDev {
   const uint8_t* lcp = nullptr;     // LCP with the previous leaf (0 for leaf 0)
 };
 
+struct FinParams {
+  int64_t Q = 0;
+  int k = 0, B = 0, S = 1;
+  const int* qslot_off = nullptr;     // [Q+1]
+  const int* qslot = nullptr;         // chunk*32 + lane for each (query, probe)
+  int flat_nchunks = 0;               // > 0: one slot per query, computed from the flat chunking
+  const uint2* cand = nullptr;
+  const int* cand_cnt = nullptr;
+  const uint32_t* group_off = nullptr;  // [n_groups+1]
+  const int32_t* ids = nullptr;         // [N] grouped, ascending within a group
+  const uint32_t* group_mult = nullptr;
+  const int32_t* group_minid = nullptr;
+  const float* unit_thr = nullptr;      // [n_units][32] or null
+  float* out_dist = nullptr;
+  int32_t* out_ids = nullptr;
+};
+
+
 enum ScanMode : int { kModeFull = 0, kModeTopk = 1 };
 
 struct ScanParams {
@@ -73,23 +91,8 @@ struct ScanParams {
   int* cand_cnt = nullptr;            // [n_units][kWarps][32]
   float* unit_thr = nullptr;          // [n_units][32] final CTA threshold per lane
   int vec4 = 1;                       // query/codebook rows 16-byte aligned
-};
-
-struct FinParams {
-  int64_t Q = 0;
-  int k = 0, B = 0, S = 1;
-  const int* qslot_off = nullptr;     // [Q+1]
-  const int* qslot = nullptr;         // chunk*32 + lane for each (query, probe)
-  int flat_nchunks = 0;               // > 0: one slot per query, computed from the flat chunking
-  const uint2* cand = nullptr;
-  const int* cand_cnt = nullptr;
-  const uint32_t* group_off = nullptr;  // [n_groups+1]
-  const int32_t* ids = nullptr;         // [N] grouped, ascending within a group
-  const uint32_t* group_mult = nullptr;
-  const int32_t* group_minid = nullptr;
-  const float* unit_thr = nullptr;      // [n_units][32] or null
-  float* out_dist = nullptr;
-  int32_t* out_ids = nullptr;
+  int fuse_fin = 0;                   // S == 1: finalize this CTA's queries in the scan kernel
+  FinParams fin;
 };
 
 // ---- launchers (kernels.cu); each returns cudaGetLastError() ----

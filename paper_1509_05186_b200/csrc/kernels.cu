@@ -246,6 +246,8 @@ __device__ void tmem_load_level0(const SmemScan& sm, const float* lut0) {
 }
 
 constexpr int kDC = 16;   // query dimensions staged per table-build pass
+constexpr int kFinWarpBytes = 2 * 8 * kTopkMax + 3 * 4 * 256 + 4 * 256 + 16;   // sizeof(FinWarp)
+constexpr int kFinRegion = kWarps * kFinWarpBytes;                             // fused finalize scratch
 
 // Table entry (level l, codeword k, query slot i): level 0 of an 8-level tree
 // lives in the global scratch row lut0 (7 levels fill shared memory).
@@ -770,6 +772,9 @@ __device__ __forceinline__ void scan_any(EmitCtx& e, const SmemScan& sm, const T
   else scan_dispatch<ROLE>(e, sm, tr, a, b, lut0g);
 }
 
+struct FinWarp;
+__device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q);
+
 template <int SS, int MTC, bool FOREST>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant__ ScanParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -783,7 +788,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   const int smem_levels = (MTmax == 8) ? 7 : MTmax;
   SmemScan sm;
   sm.tab = reinterpret_cast<float*>(smem_raw);
-  sm.thr = reinterpret_cast<unsigned*>(smem_raw + (size_t)smem_levels * 256 * 32 * 4);
+  const size_t region = ((size_t)smem_levels * 256 * 32 * 4 > (size_t)kFinRegion) ? (size_t)smem_levels * 256 * 32 * 4
+                                                                                    : (size_t)kFinRegion;
+  sm.thr = reinterpret_cast<unsigned*>(smem_raw + region);
   sm.qidx = reinterpret_cast<int*>(sm.thr + 32);
   sm.stage = reinterpret_cast<float*>(sm.qidx + 32);
   sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.stage + 32 * kDC);
@@ -879,12 +886,20 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   if (p.mode == kModeTopk) {
     p.cand_cnt[(size_t)(unit * kWarps + warp) * 32 + lane] = e.ts.cnt;
     if (warp == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + lane] = __uint_as_float(sm.thr[lane]);
+    if (p.fuse_fin) {
+      // every query of this chunk was scanned entirely by this CTA: finalize here,
+      // reusing the (now dead) table memory as per-warp scratch
+      __syncthreads();
+      FinWarp* fw = reinterpret_cast<FinWarp*>(smem_raw + (size_t)warp * kFinWarpBytes);
+      for (int i = warp; i < nq; i += kWarps) finalize_query(p.fin, *fw, sm.qidx[i]);
+    }
   }
 }
 
 size_t scan_smem_bytes(int MTmax) {
   const int levels = (MTmax == 8) ? 7 : MTmax;
-  return (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + 32 * kDC * 4 + 16;
+  const size_t tab = (size_t)levels * 256 * 32 * 4;
+  return (tab > (size_t)kFinRegion ? tab : (size_t)kFinRegion) + 32 * 4 + 32 * 4 + 32 * kDC * 4 + 16;
 }
 
 template <int SS, int MTC, bool FOREST>
@@ -944,15 +959,16 @@ __device__ void warp_bitonic_sort(unsigned long long* a, int n) {
 // ---------------------------------------------------------------------------
 constexpr int kFinCap = 256;   // candidates staged in shared memory per warp
 
-struct FinSmem {
-  uint32_t key[kFinWarps][kFinCap];
-  uint32_t grp[kFinWarps][kFinCap];
-  uint32_t mul[kFinWarps][kFinCap];
-  uint32_t hist[kFinWarps][256];
-  unsigned long long stage[kFinWarps][kTopkMax];
-  unsigned long long xs[kFinWarps][kTopkMax];   // slow-path (distance, id) keys
-  int nstage[kFinWarps];
-  uint32_t tied_g[kFinWarps];
+struct FinWarp {                // one warp's finalize scratch (shared memory)
+  unsigned long long stage[kTopkMax];
+  unsigned long long xs[kTopkMax];   // slow-path (distance, id) keys
+  uint32_t key[kFinCap];
+  uint32_t grp[kFinCap];
+  uint32_t mul[kFinCap];
+  uint32_t hist[256];
+  int nstage;
+  uint32_t tied_g;
+  uint32_t pad[2];
 };
 
 // Slots (chunk*32 + lane) of query q: explicit (IVF: one per probe) or, for the
@@ -1009,13 +1025,10 @@ struct CandSrc {
   }
 };
 
-__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_constant__ FinParams p) {
-  extern __shared__ __align__(16) unsigned char fsm_raw[];
-  FinSmem& fs = *reinterpret_cast<FinSmem*>(fsm_raw);
+// Exact top-k of query q from the candidates of all its units (one warp).
+__device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
   const float* unit_thr = p.unit_thr;
-  const int lane = lane_id(), warp = warp_id();
-  const int64_t q = (int64_t)blockIdx.x * kFinWarps + warp;
-  if (q >= p.Q) return;
+  const int lane = lane_id();
   const int k = p.k;
   const int s0 = fin_s0(p, q), s1 = fin_s1(p, q);
 
@@ -1036,9 +1049,9 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   int n = 0;
   bool overflow = false;
   {
-    uint32_t* K_ = fs.key[warp];
-    uint32_t* G_ = fs.grp[warp];
-    uint32_t* U_ = fs.mul[warp];
+    uint32_t* K_ = fw.key;
+    uint32_t* G_ = fw.grp;
+    uint32_t* U_ = fw.mul;
     for (int j = s0; j < s1 && !overflow; ++j) {
       const int slot = fin_slot(p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
@@ -1079,10 +1092,10 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   __syncwarp();
   CandSrc src;
   src.p = &p; src.q = q; src.s0 = s0; src.s1 = s1; src.in_smem = !overflow; src.n = n;
-  src.key = fs.key[warp]; src.grp = fs.grp[warp]; src.mul = fs.mul[warp]; src.thr = thr;
+  src.key = fw.key; src.grp = fw.grp; src.mul = fw.mul; src.thr = thr;
 
   // 3. weighted radix select: t = smallest distance with cumulative multiplicity >= k
-  uint32_t* hist = fs.hist[warp];
+  uint32_t* hist = fw.hist;
   uint32_t prefix = 0, pmask = 0, need = (uint32_t)k;
   bool all = false;
   for (int pass = 0; pass < 4; ++pass) {
@@ -1129,24 +1142,24 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   //    Fast path: sort only the (few) groups < t by distance; when no two of
   //    them share a distance, each group's ids (ascending) are already in
   //    (distance, id) order and are written out directly.
-  unsigned long long* stage = fs.stage[warp];
-  if (lane == 0) fs.nstage[warp] = 0;
+  unsigned long long* stage = fw.stage;
+  if (lane == 0) fw.nstage = 0;
   __syncwarp();
   uint32_t slt = 0, ntied = 0;
   src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
     if (key < t || all) {
       slt += mu;
-      const int pos = atomicAdd(&fs.nstage[warp], 1);
+      const int pos = atomicAdd(&fw.nstage, 1);
       if (pos < kTopkMax) stage[pos] = ((unsigned long long)key << 32) | g;
     } else if (key == t) {
       ntied += 1;
-      fs.tied_g[warp] = g;
+      fw.tied_g = g;
     }
   });
   slt = __reduce_add_sync(FULLMASK, slt);
   ntied = __reduce_add_sync(FULLMASK, ntied);
   __syncwarp();
-  const int ng = min(fs.nstage[warp], kTopkMax);   // groups < t (< k of them)
+  const int ng = min(fw.nstage, kTopkMax);   // groups < t (< k of them)
   {
     int np2 = 32;
     while (np2 < ng) np2 <<= 1;
@@ -1197,7 +1210,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
     for (int gi = 0; gi < ng; ++gi) {
       const uint32_t key = (uint32_t)(stage[gi] >> 32), g = (uint32_t)(stage[gi] & 0xffffffffu);
       const uint32_t o0 = __ldg(p.group_off + g), mu = __ldg(p.group_off + g + 1) - o0;
-      unsigned long long* xs = fs.xs[warp];
+      unsigned long long* xs = fw.xs;
       for (uint32_t r = lane; r < mu; r += 32)
         if (n_ids + (int)r < kTopkMax)
           xs[n_ids + r] = ((unsigned long long)key << 32) | (uint32_t)__ldg(p.ids + o0 + r);
@@ -1207,7 +1220,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
     n_ids = min(n_ids, kTopkMax);
     int np2 = 32;
     while (np2 < n_ids) np2 <<= 1;
-    unsigned long long* xs = fs.xs[warp];
+    unsigned long long* xs = fw.xs;
     for (int i = n_ids + lane; i < np2; i += 32) xs[i] = ~0ull;
     __syncwarp();
     warp_bitonic_sort(xs, np2);
@@ -1222,7 +1235,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   if (!all && ntied == 1) {
     // common case: one group holds the k-th distance -> its R smallest ids
     const uint32_t R = (uint32_t)k - slt;
-    const uint32_t g = fs.tied_g[warp];
+    const uint32_t g = fw.tied_g;
     const uint32_t o0 = __ldg(p.group_off + g), o1 = __ldg(p.group_off + g + 1);
     const uint32_t take = min(R, o1 - o0);
     for (uint32_t i = lane; i < take; i += 32) {
@@ -1271,7 +1284,7 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
       }
       sigma = w;
     }
-    if (lane == 0) fs.nstage[warp] = 0;
+    if (lane == 0) fw.nstage = 0;
     __syncwarp();
     src.each([&](uint32_t key, uint32_t g, uint32_t mu) {
       if (key != t || (uint32_t)__ldg(p.group_minid + g) > tau) return;
@@ -1279,15 +1292,15 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
       for (uint32_t o = 0; o < mu; ++o) {
         const uint32_t id = (uint32_t)__ldg(p.ids + o0 + o);
         if (id > sigma) break;
-        const int pos = atomicAdd(&fs.nstage[warp], 1);
+        const int pos = atomicAdd(&fw.nstage, 1);
         if (pos < kTopkMax) stage[pos] = id;
       }
     });
     __syncwarp();
-    const int nt = min(fs.nstage[warp], (int)R);
+    const int nt = min(fw.nstage, (int)R);
     int np2 = 32;
-    while (np2 < fs.nstage[warp] && np2 < kTopkMax) np2 <<= 1;
-    for (int i = fs.nstage[warp] + lane; i < np2; i += 32) stage[i] = ~0ull;
+    while (np2 < fw.nstage && np2 < kTopkMax) np2 <<= 1;
+    for (int i = fw.nstage + lane; i < np2; i += 32) stage[i] = ~0ull;
     __syncwarp();
     warp_bitonic_sort(stage, np2);
     for (int i = lane; i < nt && written + i < k; i += 32) {
@@ -1303,9 +1316,19 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   }
 }
 
+static_assert(sizeof(FinWarp) == kFinWarpBytes, "FinWarp layout");
+
+__global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_constant__ FinParams p) {
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  FinWarp* fw = reinterpret_cast<FinWarp*>(fsm_raw);
+  const int64_t q = (int64_t)blockIdx.x * kFinWarps + warp_id();
+  if (q >= p.Q) return;
+  finalize_query(p, fw[warp_id()], q);
+}
+
 cudaError_t launch_finalize(const FinParams& p, cudaStream_t st) {
   if (p.Q <= 0) return cudaSuccess;
-  const size_t smem = sizeof(FinSmem);
+  const size_t smem = sizeof(FinWarp) * kFinWarps;
   cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((p.Q + kFinWarps - 1) / kFinWarps);
