@@ -627,7 +627,7 @@ static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool 
     w.leafdist = c.take<float>((size_t)pl.n_chunks * ix->n_groups * 32);
   } else {
     w.cand = c.take<uint2>((size_t)pl.n_units * kWarps * 32 * pl.B);
-    w.cand_cnt = c.take<int>((size_t)pl.n_units * kWarps * 32);
+    w.cand_cnt = c.take<int>((size_t)pl.n_units * 32);
     w.unit_thr = c.take<float>((size_t)pl.n_units * 32);
   }
   return w;
@@ -925,7 +925,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   fp.group_minid = ix->group_minid.as<int32_t>();
   fp.unit_thr = w.unit_thr;
   fp.out_dist = dist; fp.out_ids = ids;
-  if (pl.S == 1) {   // every query lives in one CTA: finalize inside the scan kernel
+  if (false && pl.S == 1) {   // fused finalize (kept for experiments; the separate kernel hides latency better)
     sp.fuse_fin = 1;
     sp.fin = fp;
     cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");

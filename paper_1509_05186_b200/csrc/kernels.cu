@@ -246,7 +246,7 @@ __device__ void tmem_load_level0(const SmemScan& sm, const float* lut0) {
 }
 
 constexpr int kDC = 16;   // query dimensions staged per table-build pass
-constexpr int kFinWarpBytes = 2 * 8 * kTopkMax + 3 * 4 * 256 + 4 * 256 + 16;   // sizeof(FinWarp)
+constexpr int kFinWarpBytes = 2 * 8 * kTopkMax + 3 * 4 * 512 + 4 * 256 + 16;   // sizeof(FinWarp)
 constexpr int kFinRegion = kWarps * kFinWarpBytes;                             // fused finalize scratch
 
 // Table entry (level l, codeword k, query slot i): level 0 of an 8-level tree
@@ -602,7 +602,7 @@ struct TopkState {
   float thr;
   int cnt;
   uint2* buf;         // this lane's buffer
-  uint2* warp_buf;    // lane 0's buffer (lane L's = warp_buf + L*B)
+  uint2* warp_buf;    // lane 0's buffer of this warp (lane L's = warp_buf + L*kWarps*B)
   bool active;
 };
 
@@ -643,7 +643,7 @@ __device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr
     full &= full - 1;
     int nc; float nt;
     const int n = __shfl_sync(FULLMASK, cnt, L);
-    refresh_buffer(warp_buf + (size_t)L * B, n, k, gmult, gminid, &nc, &nt);
+    refresh_buffer(warp_buf + (size_t)L * kWarps * B, n, k, gmult, gminid, &nc, &nt);
     if (lane == L) { cnt = nc; thr = fminf(thr, nt); }
   }
   return CntThr{cnt, thr};
@@ -835,8 +835,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   e.ts.warp_buf = nullptr;
   e.ts.buf = nullptr;
   if (p.mode == kModeTopk) {
-    e.ts.warp_buf = p.cand + ((size_t)(unit * kWarps + warp) * 32) * p.B;
-    e.ts.buf = e.ts.warp_buf + (size_t)lane * p.B;
+    // candidates of (unit, lane): kWarps consecutive per-warp buffers of B entries
+    e.ts.warp_buf = p.cand + ((size_t)unit * 32 * kWarps + warp) * p.B;
+    e.ts.buf = e.ts.warp_buf + (size_t)lane * kWarps * p.B;
   }
 
   // Forest: trees T-1..1 first (per-leaf partials for this CTA's queries),
@@ -880,6 +881,56 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     tmem_fence_before();
     __syncthreads();   // partials visible / tables free for the next tree
     tmem_fence_after();
+  }
+  if (use_tmem && warp == 0) tmem_dealloc(sm.tmem);
+
+  if (p.mode == kModeTopk) {
+    // Merge the 16 warps' candidates of each lane into one list under the CTA's
+    // final threshold, in place: lane L's buffers are contiguous, so the kept
+    // entries are compacted to the front (write position <= read position).
+    int* cnt_s = reinterpret_cast<int*>(smem_raw);   // tables are dead now
+    cnt_s[warp * 32 + lane] = e.ts.cnt;
+    __syncthreads();
+    for (int L = warp; L < 32; L += kWarps) {
+      const int myc = (lane < kWarps) ? cnt_s[lane * 32 + L] : 0;
+      int inc = myc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULLMASK, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int total = __shfl_sync(FULLMASK, inc, 31);
+      const int excl = inc - myc;
+      const uint32_t tb = sm.thr[L];
+      uint2* base = p.cand + ((size_t)unit * 32 + L) * kWarps * p.B;
+      int n = 0;
+      for (int i0 = 0; i0 < total; i0 += 32) {
+        const int idx = i0 + lane;
+        int w = 0;
+#pragma unroll
+        for (int st = 8; st >= 1; st >>= 1) {
+          const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
+          if (w + st < kWarps && o <= idx) w += st;
+        }
+        const int wo = __shfl_sync(FULLMASK, excl, w & 31);
+        uint2 v = make_uint2(0xffffffffu, 0);
+        if (idx < total) v = base[(size_t)w * p.B + (idx - wo)];
+        const bool keep = (idx < total) && v.x <= tb;
+        const unsigned m = __ballot_sync(FULLMASK, keep);
+        __syncwarp();
+        if (keep) base[n + __popc(m & ((1u << lane) - 1u))] = v;
+        n += __popc(m);
+      }
+      if (lane == 0) {
+        p.cand_cnt[(size_t)unit * 32 + L] = n;
+        if (p.unit_thr) p.unit_thr[(size_t)unit * 32 + L] = __uint_as_float(tb);
+      }
+    }
+    if (p.fuse_fin) {
+      __syncthreads();
+      FinWarp* fw = reinterpret_cast<FinWarp*>(smem_raw + (size_t)warp * kFinWarpBytes);
+      for (int i = warp; i < nq; i += kWarps) finalize_query(p.fin, *fw, sm.qidx[i]);
+    }
   }
   if (use_tmem && warp == 0) tmem_dealloc(sm.tmem);
 
@@ -957,7 +1008,7 @@ __device__ void warp_bitonic_sort(unsigned long long* a, int n) {
 // ---------------------------------------------------------------------------
 // K4: finalize -- exact top-k per query over the candidates of all its units
 // ---------------------------------------------------------------------------
-constexpr int kFinCap = 256;   // candidates staged in shared memory per warp
+constexpr int kFinCap = 512;   // candidates staged in shared memory per warp
 
 struct FinWarp {                // one warp's finalize scratch (shared memory)
   unsigned long long stage[kTopkMax];
@@ -988,6 +1039,8 @@ __device__ __forceinline__ int fin_slot(const FinParams& p, int64_t q, int j) {
 
 // Enumerates the candidates of query q: smem copy when they fit, else global.
 // f(key, group, multiplicity) is called once per candidate by the owning lane.
+// Each (slot, segment) unit list holds cand_cnt[unit*32+lane] entries at
+// cand + (unit*32 + lane) * kWarps * B (compacted by the scan kernel).
 struct CandSrc {
   const FinParams* p;
   int64_t q;
@@ -1010,15 +1063,12 @@ struct CandSrc {
       const int slot = fin_slot(*p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
       for (int sg = 0; sg < p->S; ++sg) {
-        const int unit = chunk * p->S + sg;
-        for (int w = 0; w < kWarps; ++w) {
-          const size_t sb = (size_t)(unit * kWarps + w) * 32 + ln;
-          const int c = __ldg(p->cand_cnt + sb);
-          const uint2* eb = p->cand + sb * p->B;
-          for (int i = lane; i < c; i += 32) {
-            const uint2 v = eb[i];
-            if (v.x <= tb) f(v.x, v.y, __ldg(p->group_mult + v.y));
-          }
+        const size_t ul = (size_t)(chunk * p->S + sg) * 32 + ln;
+        const int c = __ldg(p->cand_cnt + ul);
+        const uint2* eb = p->cand + ul * kWarps * p->B;
+        for (int i = lane; i < c; i += 32) {
+          const uint2 v = eb[i];
+          if (v.x <= tb) f(v.x, v.y, __ldg(p->group_mult + v.y));
         }
       }
     }
@@ -1045,48 +1095,51 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
   }
   const uint32_t tb = __float_as_uint(thr);
 
-  // 2. stage candidates (<= thr) into shared memory, with their multiplicities
+  // 2. stage candidates (<= thr) into shared memory, with their multiplicities:
+  //    the query's unit lists, up to 32 lists per round loaded in parallel
   int n = 0;
   bool overflow = false;
   {
     uint32_t* K_ = fw.key;
     uint32_t* G_ = fw.grp;
     uint32_t* U_ = fw.mul;
-    for (int j = s0; j < s1 && !overflow; ++j) {
-      const int slot = fin_slot(p, q, j);
-      const int chunk = slot >> 5, ln = slot & 31;
-      for (int sg = 0; sg < p.S && !overflow; ++sg) {
-        const int unit = chunk * p.S + sg;
-        // counts of the 16 warps of this unit (one load per lane), prefix sums,
-        // then all lanes load candidates in parallel across the 16 buffers
-        const int myc = (lane < kWarps) ? __ldg(p.cand_cnt + (size_t)(unit * kWarps + lane) * 32 + ln) : 0;
-        int inc = myc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(FULLMASK, inc, o);
-          if (lane >= o) inc += y;
-        }
-        const int total = __shfl_sync(FULLMASK, inc, 31);
-        const int excl = inc - myc;
-        for (int i0 = 0; i0 < total; i0 += 32) {
-          const int idx = i0 + lane;
-          int w = 0;
-#pragma unroll
-          for (int st = 8; st >= 1; st >>= 1) {
-            const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
-            if (w + st < kWarps && o <= idx) w += st;
-          }
-          const int wo = __shfl_sync(FULLMASK, excl, w & 31);
-          uint2 v = make_uint2(0xffffffffu, 0);
-          if (idx < total) v = p.cand[((size_t)(unit * kWarps + w) * 32 + ln) * p.B + (idx - wo)];
-          const bool keep = (idx < total) && v.x <= tb;
-          const unsigned m = __ballot_sync(FULLMASK, keep);
-          const int pos = n + __popc(m & ((1u << lane) - 1u));
-          if (keep && pos < kFinCap) { K_[pos] = v.x; G_[pos] = v.y; U_[pos] = __ldg(p.group_mult + v.y); }
-          n += __popc(m);
-        }
-        if (n > kFinCap) overflow = true;
+    const int nl = (s1 - s0) * p.S;
+    for (int l0 = 0; l0 < nl && !overflow; l0 += 32) {
+      const int li = l0 + lane;
+      size_t ul = 0;
+      int myc = 0;
+      if (li < nl) {
+        const int slot = fin_slot(p, q, s0 + li / p.S);
+        ul = (size_t)((slot >> 5) * p.S + li % p.S) * 32 + (slot & 31);
+        myc = __ldg(p.cand_cnt + ul);
       }
+      int inc = myc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULLMASK, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int total = __shfl_sync(FULLMASK, inc, 31);
+      const int excl = inc - myc;
+      for (int i0 = 0; i0 < total; i0 += 32) {
+        const int idx = i0 + lane;
+        int w = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1) {
+          const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
+          if (w + st < 32 && o <= idx) w += st;
+        }
+        const int wo = __shfl_sync(FULLMASK, excl, w);
+        const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
+        uint2 v = make_uint2(0xffffffffu, 0);
+        if (idx < total) v = p.cand[ulw * kWarps * p.B + (idx - wo)];
+        const bool keep = (idx < total) && v.x <= tb;
+        const unsigned m = __ballot_sync(FULLMASK, keep);
+        const int pos = n + __popc(m & ((1u << lane) - 1u));
+        if (keep && pos < kFinCap) { K_[pos] = v.x; G_[pos] = v.y; U_[pos] = __ldg(p.group_mult + v.y); }
+        n += __popc(m);
+      }
+      if (n > kFinCap) overflow = true;
     }
   }
   __syncwarp();
