@@ -932,19 +932,6 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       for (int i = warp; i < nq; i += kWarps) finalize_query(p.fin, *fw, sm.qidx[i]);
     }
   }
-  if (use_tmem && warp == 0) tmem_dealloc(sm.tmem);
-
-  if (p.mode == kModeTopk) {
-    p.cand_cnt[(size_t)(unit * kWarps + warp) * 32 + lane] = e.ts.cnt;
-    if (warp == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + lane] = __uint_as_float(sm.thr[lane]);
-    if (p.fuse_fin) {
-      // every query of this chunk was scanned entirely by this CTA: finalize here,
-      // reusing the (now dead) table memory as per-warp scratch
-      __syncthreads();
-      FinWarp* fw = reinterpret_cast<FinWarp*>(smem_raw + (size_t)warp * kFinWarpBytes);
-      for (int i = warp; i < nq; i += kWarps) finalize_query(p.fin, *fw, sm.qidx[i]);
-    }
-  }
 }
 
 size_t scan_smem_bytes(int MTmax) {
