@@ -925,6 +925,8 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   fp.group_minid = ix->group_minid.as<int32_t>();
   fp.unit_thr = w.unit_thr;
   fp.out_dist = dist; fp.out_ids = ids;
+  // register fast path when groups are large (few candidates per query)
+  fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
   if (false && pl.S == 1) {   // fused finalize (kept for experiments; the separate kernel hides latency better)
     sp.fuse_fin = 1;
     sp.fin = fp;
@@ -993,6 +995,7 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   fp.group_minid = ix->group_minid.as<int32_t>();
   fp.unit_thr = w.unit_thr;
   fp.out_dist = dist; fp.out_ids = ids;
+  fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
   cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
   ET_API_END
 }

@@ -47,6 +47,9 @@ struct FinParams {
   const float* unit_thr = nullptr;      // [n_units][32] or null
   float* out_dist = nullptr;
   int32_t* out_ids = nullptr;
+  // two-tier finalize: a register fast path for few candidates per query; the
+  // shared-memory path (finalize_query) for the rest (kernels.cu)
+  int fast = 0;
 };
 
 

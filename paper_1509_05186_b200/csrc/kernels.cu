@@ -306,54 +306,99 @@ __device__ __forceinline__ void build_pass_generic(const SmemScan& sm, float* lu
   }
 }
 
-// Resident-staging build for s == 16 (every d = 128 configuration): the
-// active queries' sub-vectors of levels 0..MT-2 are staged once into the
-// shared-memory region of the tree's LAST level (not built yet), those levels
-// are built without barriers, then the last level is built from the small
-// stage.  Three barriers per tree instead of two per pass.
+// Packed fp32x2 arithmetic (sm_100a FADD2 / FFMA2): two independent IEEE fp32
+// operations per instruction, each rounded exactly like the scalar op, so an
+// entry computed two-queries-at-a-time equals the scalar j-ascending chain.
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long f2sub(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2sqacc(unsigned long long t, unsigned long long acc) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(t), "l"(acc));
+  return r;
+}
+
+// Copy one table (smem region, swizzled [k][lane ^ (k & 31)]) into every warp
+// quadrant's TMEM lanes: warp w copies 64 columns for quadrant w & 3.
+__device__ __forceinline__ void tmem_load_from_smem(const SmemScan& sm, uint32_t region_s) {
+  const int lane = lane_id(), warp = warp_id();
+  const int sub = warp >> 2;
+  const uint32_t tb = tmem_lane_base(sm.tmem);
+  const uint32_t lane4 = (uint32_t)lane << 2;
+  for (int c0 = sub * 64; c0 < sub * 64 + 64; c0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = lds(tab_addr(region_s, 0, (uint32_t)(c0 + j), lane4));
+    tmem_st8(tb + (uint32_t)c0, v);
+  }
+  tmem_wait_st();
+}
+
+// Resident-staging table build for s == 16 (every d = 128 configuration).
+// The active queries' sub-vectors are staged ONCE, as query pairs
+// [level][pair][dim][2], levels 0..MT-2 into the shared-memory region of the
+// tree's last level (built last) and level MT-1 into the small stage.  Warp w
+// owns codeword block kb = (w >> 1) & 7 (lane = codeword) and query-pair half
+// g = w & 1; for each level it keeps its codeword in registers and runs two
+// packed FADD2/FFMA2 chains (two query pairs, four entries) at a time against
+// broadcast LDS.128 loads of the staged pairs.  With 8 levels, level 0 is
+// built first into the region of level 6 and copied to TMEM.
 template <int SS, int MT>
 __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq,
                                       int cell) {
   static_assert(SS == kDC, "resident staging handles s == 16");
   const TreeDev& tr = p.tree[t];
-  const int lv0 = (MT == 8) ? 1 : 0;
+  constexpr int lv0 = (MT == 8) ? 1 : 0;   // level 0 of an 8-level tree lives in TMEM
   const int K = p.K, d = p.d;
-  const int nb = (K + 31) >> 5;
   const int lane = lane_id(), warp = warp_id();
-  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
   const uint32_t tab_s = smem_u32(sm.tab);
   const uint32_t region_s = tab_s + ((uint32_t)(MT - 1 - lv0) << 15);   // last level's table region
   const uint32_t stage_s = smem_u32(sm.stage);
-  const uint32_t dsm_s = smem_u32(et_dsm);                               // offsets for lds4_off
-  // ---- stage: levels 0..MT-2 -> region [l][i][16]; level MT-1 -> stage [i][16]
-  const int per_level = nq * SS;
+  const int np = (nq + 1) >> 1;                                          // query pairs
+  const uint32_t pair_bytes = SS * 2 * 4;                                // 128 B per (level, pair)
   __syncthreads();                                   // previous tree's scan is done with the tables
   {
-    // thread t stages dimension j = t % 16 of query slot i = t / 16 for every
-    // level: all loads first (independent), then the stores
+    // thread -> (query slot i, dim j); all loads first, then the stores.  The
+    // odd partner of an odd nq is staged as 0 (its entries are never stored).
     const int i = threadIdx.x >> 4, j = threadIdx.x & (SS - 1);
-    if (i < nq) {
-      const int q = sm.qidx[i];
-      const float* xr = p.queries + (size_t)q * d + j;
-      const float* cr = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + j : nullptr;
+    if (i < nq + (nq & 1)) {
       float v[MT];
+      if (i < nq) {
+        const int q = sm.qidx[i];
+        const float* xr = p.queries + (size_t)q * d + j;
+        const float* cr = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + j : nullptr;
 #pragma unroll
-      for (int l = 0; l < MT; ++l) v[l] = __ldg(xr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
-      if (cr) {
+        for (int l = 0; l < MT; ++l) v[l] = __ldg(xr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
+        if (cr) {
 #pragma unroll
-        for (int l = 0; l < MT; ++l) v[l] -= __ldg(cr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
+          for (int l = 0; l < MT; ++l) v[l] -= __ldg(cr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
+        }
+      } else {
+#pragma unroll
+        for (int l = 0; l < MT; ++l) v[l] = 0.f;
       }
+      const uint32_t o = (uint32_t)(i >> 1) * pair_bytes + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
 #pragma unroll
-      for (int l = 0; l < MT - 1; ++l) sts(region_s + 4u * (uint32_t)(l * per_level + i * SS + j), v[l]);
-      sts(stage_s + 4u * (uint32_t)(i * SS + j), v[MT - 1]);
+      for (int l = 0; l < MT - 1; ++l) sts(region_s + (uint32_t)(l * np) * pair_bytes + o, v[l]);
+      sts(stage_s + o, v[MT - 1]);
     }
   }
-  __syncthreads();
-  const int G = max(1, kWarps / nb);
-  const uint32_t lane4 = (uint32_t)lane << 2;
-  auto load_cw = [&](int l, int kb, float (&c)[SS]) {
-    const int k = kb * 32 + lane;
-    const bool kvalid = k < K;
+  const int kb = (warp >> 1) & 7, g = warp & 1;
+  const int k = kb * 32 + lane;
+  const bool kvalid = k < K;
+  const int p0 = g ? (np + 1) >> 1 : 0, p1 = g ? np : (np + 1) >> 1;
+  const bool active = kb * 32 < K;                   // K < 256: idle codeword blocks
+  auto load_cw = [&](int l, float (&c)[SS]) {
     const int m = p.layer_sub[tr.layer0 + l];
     const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
 #pragma unroll
@@ -362,65 +407,76 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
       c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
     }
   };
-  auto item = [&](int l, int kb, int g, uint32_t xs_s, const float (&c)[SS]) {
-    const uint32_t k = (uint32_t)(kb * 32 + lane);
-    const bool kvalid = (int)k < K;
+  // entries of level-slot `dst` (table region index) for pairs [p0, p1) of stage xs
+  auto item = [&](uint32_t dst_s, uint32_t xs_s, const float (&c)[SS]) {
+    const uint32_t lane4 = (uint32_t)lane << 2;
     auto put = [&](int i, float a) {
-      if (!kvalid) return;
-      if (l < lv0) lut0[k * 32 + i] = a;
-      else sts(tab_addr(tab_s, l - lv0, k, (uint32_t)i << 2), a);
+      if (kvalid && i < nq) sts(tab_addr(dst_s, 0, (uint32_t)k, (uint32_t)i << 2), a);
     };
-    int i = g;
-    for (; i + G < nq; i += 2 * G) {
-      const uint32_t x0 = xs_s - dsm_s + (uint32_t)i * (SS * 4);
-      const uint32_t x1 = xs_s - dsm_s + (uint32_t)(i + G) * (SS * 4);
-      float a0 = 0.f, a1 = 0.f;
+    (void)lane4;
+    int pi = p0;
+    for (; pi + 1 < p1; pi += 2) {
+      const uint32_t x0 = xs_s + (uint32_t)pi * pair_bytes, x1 = x0 + pair_bytes;
+      unsigned long long a0 = 0ull, a1 = 0ull;
 #pragma unroll
-      for (int j = 0; j < SS; j += 4) {
-        const float4 u0 = lds4_off(x0 + 4 * j), u1 = lds4_off(x1 + 4 * j);
-        float t0, t1;
-        t0 = u0.x - c[j];     t1 = u1.x - c[j];     a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
-        t0 = u0.y - c[j + 1]; t1 = u1.y - c[j + 1]; a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
-        t0 = u0.z - c[j + 2]; t1 = u1.z - c[j + 2]; a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
-        t0 = u0.w - c[j + 3]; t1 = u1.w - c[j + 3]; a0 = fmaf(t0, t0, a0); a1 = fmaf(t1, t1, a1);
+      for (int j = 0; j < SS; j += 2) {
+        const float4 u0 = lds4(x0 + (uint32_t)j * 8u), u1 = lds4(x1 + (uint32_t)j * 8u);
+        const unsigned long long cj = f2pack(c[j], c[j]), cj1 = f2pack(c[j + 1], c[j + 1]);
+        unsigned long long t0 = f2sub(f2pack(u0.x, u0.y), cj), t1 = f2sub(f2pack(u1.x, u1.y), cj);
+        a0 = f2sqacc(t0, a0); a1 = f2sqacc(t1, a1);
+        t0 = f2sub(f2pack(u0.z, u0.w), cj1); t1 = f2sub(f2pack(u1.z, u1.w), cj1);
+        a0 = f2sqacc(t0, a0); a1 = f2sqacc(t1, a1);
       }
-      put(i, a0);
-      put(i + G, a1);
+      float e0, o0, e1, o1;
+      f2unpack(a0, e0, o0);
+      f2unpack(a1, e1, o1);
+      put(2 * pi, e0); put(2 * pi + 1, o0); put(2 * pi + 2, e1); put(2 * pi + 3, o1);
     }
-    if (i < nq) {
-      const uint32_t x0 = xs_s - dsm_s + (uint32_t)i * (SS * 4);
-      float a0 = 0.f;
+    if (pi < p1) {
+      const uint32_t x0 = xs_s + (uint32_t)pi * pair_bytes;
+      unsigned long long a0 = 0ull;
 #pragma unroll
-      for (int j = 0; j < SS; j += 4) {
-        const float4 u0 = lds4_off(x0 + 4 * j);
-        float t0;
-        t0 = u0.x - c[j];     a0 = fmaf(t0, t0, a0);
-        t0 = u0.y - c[j + 1]; a0 = fmaf(t0, t0, a0);
-        t0 = u0.z - c[j + 2]; a0 = fmaf(t0, t0, a0);
-        t0 = u0.w - c[j + 3]; a0 = fmaf(t0, t0, a0);
+      for (int j = 0; j < SS; j += 2) {
+        const float4 u0 = lds4(x0 + (uint32_t)j * 8u);
+        a0 = f2sqacc(f2sub(f2pack(u0.x, u0.y), f2pack(c[j], c[j])), a0);
+        a0 = f2sqacc(f2sub(f2pack(u0.z, u0.w), f2pack(c[j + 1], c[j + 1])), a0);
       }
-      put(i, a0);
+      float e0, o0;
+      f2unpack(a0, e0, o0);
+      put(2 * pi, e0); put(2 * pi + 1, o0);
     }
   };
-  const int per = nb * G;
-  const int n_items = (MT - 1) * per;
   float cw[SS], cwn[SS];
-  int it = warp;
-  if (it < n_items) load_cw(it / per, (it % per) % nb, cw);
-  for (; it < n_items; it += kWarps) {
-    const int l = it / per, r = it - l * per;
-    const int nx = it + kWarps;
-    if (nx < n_items) load_cw(nx / per, (nx % per) % nb, cwn);   // prefetch the next item's codeword
-    item(l, r % nb, r / nb, region_s + ((uint32_t)l * per_level) * 4u, cw);
+  if (active) load_cw(0, cw);
+  __syncthreads();                                   // stage complete
+  if constexpr (MT == 8) {
+    // level 0 -> region of level 6 (free until level 6 is built) -> TMEM
+    const uint32_t l0_s = tab_s + (5u << 15);
+    if (active) {
+      load_cw(1, cwn);
+      item(l0_s, region_s, cw);
 #pragma unroll
-    for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
+      for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
+    }
+    __syncthreads();
+    tmem_fence_after();
+    tmem_load_from_smem(sm, l0_s);
+    tmem_fence_before();
+    __syncthreads();
+  }
+  // levels lv0 .. MT-2 (their queries staged in the last level's region)
+  if (active) {
+    for (int l = lv0; l < MT - 1; ++l) {
+      if (l + 1 < MT) load_cw(l + 1, cwn);           // prefetch the next level's codeword
+      item(tab_s + ((uint32_t)(l - lv0) << 15), region_s + (uint32_t)(l * np) * pair_bytes, cw);
+#pragma unroll
+      for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
+    }
   }
   __syncthreads();                                   // region free: build the last level into it
-  for (int it2 = warp; it2 < per; it2 += kWarps) {
-    load_cw(MT - 1, it2 % nb, cw);
-    item(MT - 1, it2 % nb, it2 / nb, stage_s, cw);
-  }
+  if (active) item(region_s, stage_s, cw);
   __syncthreads();
+  if constexpr (MT == 8) tmem_fence_after();         // TMEM level 0 visible to the scan's tcgen05.ld
 }
 
 // Build the tables of tree t for this CTA's queries (fused).
@@ -844,14 +900,15 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   // then tree 0, whose leaves walk their tuples and sum in tree order.
   for (int t = p.T - 1; t >= 0; --t) {
     const TreeDev& tr = p.tree[t];
+    bool level0_done = false;   // resident build copies level 0 to TMEM itself
     if constexpr (SS == kDC && MTC > 0) {
       if (p.luts) { build_tables<SS>(p, sm, t, unit, nq, cell); __syncthreads(); }
-      else build_tables_resident<SS, MTC>(p, sm, t, unit, nq, cell);
+      else { build_tables_resident<SS, MTC>(p, sm, t, unit, nq, cell); level0_done = true; }
     } else {
       build_tables<SS>(p, sm, t, unit, nq, cell);
       __syncthreads();
     }
-    if (tr.MT == 8) {   // level 0 -> TMEM (every warp copies a quarter of its quadrant's columns)
+    if (tr.MT == 8 && !level0_done) {   // level 0 -> TMEM (every warp copies a quarter of its quadrant's columns)
       tmem_fence_after();
       tmem_load_level0(sm, lut0g);
       tmem_fence_before();
@@ -1014,8 +1071,15 @@ struct FinWarp {                // one warp's finalize scratch (shared memory)
 __device__ __forceinline__ int fin_s0(const FinParams& p, int64_t q) { return p.flat_nchunks ? 0 : p.qslot_off[q]; }
 __device__ __forceinline__ int fin_s1(const FinParams& p, int64_t q) { return p.flat_nchunks ? 1 : p.qslot_off[q + 1]; }
 __device__ __forceinline__ int fin_slot(const FinParams& p, int64_t q, int j) {
-  if (p.flat_nchunks) {
+  if (p.flat_nchunks) {   // chunk c holds queries [c*Q/n, (c+1)*Q/n)
     const int64_t n = p.flat_nchunks, Q = p.Q;
+    if (Q * n < (1ll << 32)) {   // 32-bit arithmetic (the common case)
+      const uint32_t Qu = (uint32_t)Q, nu = (uint32_t)n, qu = (uint32_t)q;
+      uint32_t c = (uint32_t)(((uint64_t)qu * nu) / Qu);
+      while (c + 1 < nu && (c + 1) * Qu / nu <= qu) ++c;
+      while (c > 0 && c * Qu / nu > qu) --c;
+      return (int)(c * 32 + (qu - c * Qu / nu));
+    }
     int64_t c = q * n / Q;
     while (c + 1 < n && (c + 1) * Q / n <= q) ++c;
     while (c > 0 && c * Q / n > q) --c;
@@ -1366,8 +1430,226 @@ __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_c
   finalize_query(p, fw[warp_id()], q);
 }
 
+// ---------------------------------------------------------------------------
+// K4 fast path: the same exact top-k, with the query's surviving candidates
+// (<= kFastCap) held in registers -- no shared memory, so many warps per SM
+// hide the few dependent global loads.  It decides the query only when every
+// selected group has a distinct distance (then each group's ascending ids are
+// already in (distance, id) order); otherwise -- or with more candidates --
+// the warp runs the shared-memory slow path (finalize_query) under a CTA lock.
+// ---------------------------------------------------------------------------
+constexpr int kFastCap = 64;       // 2 candidates per lane
+constexpr int kFastWarps = 8;
+
+// Ascending bitonic sort of 64 keys held as element e = r * 32 + lane in register r.
+__device__ __forceinline__ void bitonic64(unsigned long long& a0, unsigned long long& a1) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride == 32) {   // size == 64: partner is the other register of this lane
+        const unsigned long long x = a0, y = a1;
+        if (x > y) { a0 = y; a1 = x; }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          unsigned long long& a = r ? a1 : a0;
+          const int e = r * 32 + lane;
+          const unsigned long long o = __shfl_xor_sync(FULLMASK, a, stride);
+          const bool up = (e & size) == 0;
+          const bool lower = (e & stride) == 0;
+          a = (lower == up) ? (a < o ? a : o) : (a > o ? a : o);
+        }
+      }
+    }
+  }
+}
+
+// Slow path inside the fast kernel: the CTA's one FinWarp scratch, taken under
+// a CTA lock (rare: more than kFastCap candidates or exact distance ties).
+__device__ __noinline__ void finalize_locked(const FinParams& p, int64_t q) {
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  FinWarp* fw = reinterpret_cast<FinWarp*>(fsm_raw + 16);
+  int* lock = reinterpret_cast<int*>(fsm_raw);
+  if (lane_id() == 0) while (atomicCAS(lock, 0, 1) != 0) __nanosleep(64);
+  __syncwarp();
+  __threadfence_block();
+  finalize_query(p, *fw, q);
+  __threadfence_block();
+  __syncwarp();
+  if (lane_id() == 0) atomicExch(lock, 0);
+}
+
+// Ascending bitonic sort of 32 keys, one per lane.
+__device__ __forceinline__ void bitonic32(unsigned long long& a) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(FULLMASK, a, stride);
+      const bool up = (lane & size) == 0 || size == 32;
+      const bool lower = (lane & stride) == 0;
+      a = (lower == up) ? (a < o ? a : o) : (a > o ? a : o);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __grid_constant__ FinParams p) {
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  if (threadIdx.x == 0) *reinterpret_cast<int*>(fsm_raw) = 0;
+  __syncthreads();
+  const int lane = lane_id();
+  const int64_t q = (int64_t)blockIdx.x * kFastWarps + warp_id();
+  if (q >= p.Q) return;
+  const int k = p.k;
+  const int s0 = fin_s0(p, q), s1 = fin_s1(p, q);
+
+  // 1. threshold prefilter (as the slow path)
+  float thr = __int_as_float(0x7f800000);
+  if (p.unit_thr) {
+    for (int j = s0; j < s1; ++j) {
+      const int slot = fin_slot(p, q, j);
+      const int chunk = slot >> 5, ln = slot & 31;
+      for (int sg = lane; sg < p.S; sg += 32)
+        thr = fminf(thr, __ldg(p.unit_thr + (size_t)(chunk * p.S + sg) * 32 + ln));
+    }
+    for (int o = 16; o > 0; o >>= 1) thr = fminf(thr, __shfl_xor_sync(FULLMASK, thr, o));
+  }
+  const uint32_t tb = __float_as_uint(thr);
+
+  // 2. gather the candidates <= thr into registers: position i -> lane i & 31, register i >> 5
+  uint2 r0 = make_uint2(0xffffffffu, 0), r1 = make_uint2(0xffffffffu, 0);
+  int n = 0;
+  bool overflow = false;
+  const int nl = (s1 - s0) * p.S;
+  for (int l0 = 0; l0 < nl && !overflow; l0 += 32) {
+    const int li = l0 + lane;
+    size_t ul = 0;
+    int myc = 0;
+    if (li < nl) {
+      const int slot = fin_slot(p, q, s0 + li / p.S);
+      ul = (size_t)((slot >> 5) * p.S + li % p.S) * 32 + (slot & 31);
+      myc = __ldg(p.cand_cnt + ul);
+    }
+    int inc = myc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULLMASK, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int total = __shfl_sync(FULLMASK, inc, 31);
+    const int excl = inc - myc;
+    for (int i0 = 0; i0 < total; i0 += 32) {
+      const int idx = i0 + lane;
+      int w = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
+        if (w + st < 32 && o <= idx) w += st;
+      }
+      const int wo = __shfl_sync(FULLMASK, excl, w);
+      const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
+      uint2 v = make_uint2(0xffffffffu, 0);
+      if (idx < total) v = p.cand[ulw * kWarps * p.B + (idx - wo)];
+      const bool keep = (idx < total) && v.x <= tb;
+      const unsigned m = __ballot_sync(FULLMASK, keep);
+      const int c = __popc(m);
+      if (n + c > kFastCap) { overflow = true; break; }
+      // lane L receives the r-th kept entry, r = (L - n) mod 32, at position n + r
+      const int r = (lane - n) & 31;
+      const int src = (r < c) ? (int)__fns(m, 0, r + 1) : 0;
+      const uint32_t vx = __shfl_sync(FULLMASK, v.x, src);
+      const uint32_t vy = __shfl_sync(FULLMASK, v.y, src);
+      if (r < c) {
+        if (((n + r) >> 5) == 0) r0 = make_uint2(vx, vy); else r1 = make_uint2(vx, vy);
+      }
+      n += c;
+    }
+  }
+  if (overflow) { finalize_locked(p, q); return; }
+
+  // 3. offsets / multiplicities of the held groups (one dependent load)
+  uint32_t o0a = 0, mua = 0, o0b = 0, mub = 0;
+  if (lane < n) { o0a = __ldg(p.group_off + r0.y); mua = __ldg(p.group_off + r0.y + 1) - o0a; }
+  if (32 + lane < n) { o0b = __ldg(p.group_off + r1.y); mub = __ldg(p.group_off + r1.y + 1) - o0b; }
+
+  // 4. sort by (distance, position); unused positions sort last
+  unsigned long long a0 = ((unsigned long long)r0.x << 32) | (uint32_t)lane;
+  unsigned long long a1 = ((unsigned long long)r1.x << 32) | (uint32_t)(32 + lane);
+  if (lane >= n) a0 = ~0ull;
+  if (32 + lane >= n) a1 = ~0ull;
+  if (n > 32) bitonic64(a0, a1);
+  else if (n > 1) bitonic32(a0);
+  auto payload = [&](unsigned long long a, uint32_t& off, uint32_t& mu) {
+    const uint32_t pos = (uint32_t)(a & 63u);
+    const uint32_t hl = pos & 31u;
+    const uint32_t oa = __shfl_sync(FULLMASK, o0a, hl), ob = __shfl_sync(FULLMASK, o0b, hl);
+    const uint32_t ma = __shfl_sync(FULLMASK, mua, hl), mb = __shfl_sync(FULLMASK, mub, hl);
+    off = (pos >> 5) ? ob : oa;
+    mu = (a == ~0ull) ? 0u : ((pos >> 5) ? mb : ma);
+  };
+  uint32_t offA, muA, offB, muB;
+  payload(a0, offA, muA);
+  payload(a1, offB, muB);
+  uint32_t cA = muA, cB = muB;   // inclusive prefix of multiplicities, sorted order
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t ya = __shfl_up_sync(FULLMASK, cA, o), yb = __shfl_up_sync(FULLMASK, cB, o);
+    if (lane >= o) { cA += ya; cB += yb; }
+  }
+  cB += __shfl_sync(FULLMASK, cA, 31);
+  // last selected element: the first with cumulative multiplicity >= k (else all n)
+  const unsigned hitA = __ballot_sync(FULLMASK, lane < n && cA >= (uint32_t)k);
+  const unsigned hitB = __ballot_sync(FULLMASK, 32 + lane < n && cB >= (uint32_t)k);
+  const int last = hitA ? (__ffs(hitA) - 1) : (hitB ? 32 + __ffs(hitB) - 1 : n - 1);
+  // an exact distance tie among the selected elements, or between the last one
+  // and the next, needs the id-level merge of the slow path
+  const uint32_t dA = (uint32_t)(a0 >> 32), dB = (uint32_t)(a1 >> 32);
+  const uint32_t dA_next = __shfl_down_sync(FULLMASK, dA, 1);
+  const uint32_t dB_first = __shfl_sync(FULLMASK, dB, 0);
+  const uint32_t dB_next = __shfl_down_sync(FULLMASK, dB, 1);
+  const uint32_t nA = (lane == 31) ? dB_first : dA_next;
+  const bool tieA = (lane <= last) && (lane + 1 < n) && nA == dA;
+  const bool tieB = (32 + lane <= last) && (32 + lane + 1 < n) && lane < 31 && dB_next == dB;
+  if (__any_sync(FULLMASK, tieA || tieB)) { finalize_locked(p, q); return; }
+
+  // 5. output: the selected groups in distance order, ids ascending within each
+  float* od = p.out_dist + (size_t)q * k;
+  int32_t* oi = p.out_ids + (size_t)q * k;
+  for (int e = 0; e <= last; ++e) {
+    const int r = e >> 5, L = e & 31;
+    const uint32_t d = __shfl_sync(FULLMASK, r ? dB : dA, L);
+    const uint32_t off = __shfl_sync(FULLMASK, r ? offB : offA, L);
+    const uint32_t mu = __shfl_sync(FULLMASK, r ? muB : muA, L);
+    const uint32_t cum = __shfl_sync(FULLMASK, r ? cB : cA, L);
+    const uint32_t base = cum - mu;
+    const uint32_t take = min(mu, (uint32_t)k - base);
+    for (uint32_t i = lane; i < take; i += 32) {
+      od[base + i] = __uint_as_float(d);
+      oi[base + i] = __ldg(p.ids + off + i);
+    }
+  }
+  uint32_t written = 0;
+  if (last >= 0) written = __shfl_sync(FULLMASK, (last >> 5) ? cB : cA, last & 31);
+  written = min(written, (uint32_t)k);
+  for (uint32_t i = written + lane; i < (uint32_t)k; i += 32) {
+    od[i] = __int_as_float(0x7f800000);
+    oi[i] = -1;
+  }
+}
+
 cudaError_t launch_finalize(const FinParams& p, cudaStream_t st) {
   if (p.Q <= 0) return cudaSuccess;
+  if (p.fast) {
+    const size_t smem = sizeof(FinWarp) + 16;
+    cudaError_t e = cudaFuncSetAttribute(finalize_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    finalize_fast_kernel<<<(unsigned)((p.Q + kFastWarps - 1) / kFastWarps), kFastWarps * 32, smem, st>>>(p);
+    count_launch();
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(FinWarp) * kFinWarps;
   cudaError_t e = cudaFuncSetAttribute(finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
