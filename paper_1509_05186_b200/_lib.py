@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libetree.so")
+LIB_PATH = os.environ.get("ET_LIB_PATH") or os.path.join(HERE, "_build", "libetree.so")  # override: experiment builds
 
 ET_STATUS = {
     0: "ET_OK", 1: "ET_ERR_INSUFFICIENT_DATA", 2: "ET_ERR_SUBSPACE_SPLIT",

@@ -224,7 +224,7 @@ static void tree_stats(HostTree& t, int64_t N) {
   t.st.lookups = look;
   t.st.L2_records = recs;
   t.st.paper_bytes = 4 * N + 2 * (L1 + recs) + post_recs;
-  t.st.device_bytes = L2 * 17;
+  t.st.device_bytes = L2 * 16;   // leaf records (make_records)
 }
 
 static void check_codes(const uint8_t* codes, int64_t n, int M, int K) {
@@ -276,28 +276,33 @@ static void upload_groups(et_index* ix, const Groups& g, const std::vector<uint3
   if (!slot2group.empty()) ix->slot2group.upload(slot2group);
 }
 
-// Leaf records of the device layout: for each level l the
-// pre-swizzled byte offset of table entry (l, k = code byte l) inside that
-// level's 32 KB shared-memory table, (k << 7) | ((k & 31) << 2), so a lookup is
-// one XOR with the lane's offset; level 0 of an 8-level tree (held in TMEM)
-// stores the raw column k.
-static std::vector<uint4> make_records(const std::vector<uint64_t>& code, int MT) {
-  std::vector<uint4> rec(code.size());
-  for (size_t i = 0; i < code.size(); ++i) {
-    uint16_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+// Leaf records of the device layout: one uint4 = 8
+// half-words; half-word l = the pre-swizzled byte offset of table entry
+// (l, k = code byte l) inside that level's 32 KB shared-memory table,
+// (k << 7) | ((k & 31) << 2), so a lookup is one XOR with the lane's offset.
+// Level 0 of an 8-level tree (held in TMEM) stores the column k with the LCP
+// with the previous leaf in bits 8..11; shorter trees keep the LCP in
+// half-word 7.
+static std::vector<uint4> make_records(const HostTree& h) {
+  const int MT = h.MT;
+  std::vector<uint4> rec(h.code.size());
+  for (size_t i = 0; i < h.code.size(); ++i) {
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int l = 0; l < MT; ++l) {
-      const uint32_t k = (uint32_t)((code[i] >> (8 * l)) & 255u);
-      w[l] = (MT == 8 && l == 0) ? (uint16_t)k : (uint16_t)((k << 7) | ((k & 31u) << 2));
+      const uint32_t k = (uint32_t)((h.code[i] >> (8 * l)) & 255u);
+      w[l] = (MT == 8 && l == 0) ? k : ((k << 7) | ((k & 31u) << 2));
     }
-    rec[i] = make_uint4(w[0] | ((uint32_t)w[1] << 16), w[2] | ((uint32_t)w[3] << 16),
-                        w[4] | ((uint32_t)w[5] << 16), w[6] | ((uint32_t)w[7] << 16));
+    const uint32_t lcp = (i < h.lcp.size()) ? h.lcp[i] : 0u;
+    if (MT == 8) w[0] |= lcp << 8;
+    else w[7] = lcp;
+    rec[i] = make_uint4(w[0] | (w[1] << 16), w[2] | (w[3] << 16), w[4] | (w[5] << 16), w[6] | (w[7] << 16));
   }
   return rec;
 }
 
 static void finish_tree(et_index* ix, int t, HostTree& h) {
   ix->n_leaves[t] = (int64_t)h.code.size();
-  ix->code[t].upload(make_records(h.code, h.MT));
+  ix->code[t].upload(make_records(h));
   ix->lcp[t].upload(h.lcp);
   ix->stats[t] = h.st;
 }
@@ -435,7 +440,7 @@ static et_index* build_flat(const uint8_t* codes, const int32_t* ids, int64_t n,
   h.lcp.assign(n, 0);
   h.mult.assign(n, 1);
   for (int64_t i = 0; i < n; ++i) h.code[i] = pack(codes + (size_t)i * M, 0, M);
-  h.st.N = n; h.st.M = M; h.st.L2 = n; h.st.lookups = n * M; h.st.device_bytes = n * 17;
+  h.st.N = n; h.st.M = M; h.st.L2 = n; h.st.lookups = n * M; h.st.device_bytes = n * 16;
   h.st.L2_records = n; h.st.total_postfix = n * (M - 1); h.st.paper_bytes = 4 * n + n * M;
   finish_tree(ix.get(), 0, h);
   Groups g;
@@ -491,11 +496,12 @@ static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t 
         const uint64_t pk = pack(codes_in + (size_t)r * M, 0, M);
         const uint8_t lp = i == 0 ? 0 : (uint8_t)row_lcp(codes_in, M, so[i - 1], r, 0, M);
         lt.code.push_back(pk); lt.lcp.push_back(lp); lt.mult.push_back(0);
-        h.code.push_back(pk); h.lcp.push_back(lp);
+        h.code.push_back(pk); h.lcp.push_back(lp); h.mult.push_back(0);
         g.off.push_back((uint32_t)g.ids.size());
         g.first.push_back(r);
       }
       lt.mult.back() += 1;
+      h.mult.back() += 1;
       s2g[r] = (uint32_t)(h.code.size() - 1);
       g.ids.push_back(ids ? ids[r] : (int32_t)r);
     }
@@ -509,10 +515,10 @@ static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t 
     for (size_t j = 0; j + 1 < g.off.size(); ++j) std::sort(g.ids.begin() + g.off[j], g.ids.begin() + g.off[j + 1]);
   }
   upload_groups(ix.get(), g, s2g);
-  tot.N = n; tot.M = M; tot.device_bytes = (int64_t)h.code.size() * 17;
+  tot.N = n; tot.M = M; tot.device_bytes = (int64_t)h.code.size() * 16;
   tot.groups = (int64_t)(g.off.size() - 1);
   ix->n_leaves[0] = (int64_t)h.code.size();
-  ix->code[0].upload(make_records(h.code, M));
+  ix->code[0].upload(make_records(h));
   ix->lcp[0].upload(h.lcp);
   ix->stats[0] = tot;
   ix->list_leaf_off_d.upload(ix->list_leaf_off);
@@ -614,6 +620,7 @@ struct Work {
   int* chunk_q; int* qslot_off; int* qslot;
   float* lut0; float* partials; float* leafdist;
   uint2* cand; int* cand_cnt; float* unit_thr;
+  unsigned* qthr;
 };
 
 static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool full, int slots_per_q) {
@@ -629,6 +636,7 @@ static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool 
     w.cand = c.take<uint2>((size_t)pl.n_units * kWarps * 32 * pl.B);
     w.cand_cnt = c.take<int>((size_t)pl.n_units * 32);
     w.unit_thr = c.take<float>((size_t)pl.n_units * 32);
+    w.qthr = c.take<unsigned>((size_t)Q);
   }
   return w;
 }
@@ -915,6 +923,8 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   sp.cand = w.cand;
   sp.cand_cnt = w.cand_cnt;
   sp.unit_thr = w.unit_thr;
+  sp.qthr = w.qthr;
+  cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, (cudaStream_t)stream), "qthr init");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
   fp.flat_nchunks = pl.n_chunks;
@@ -924,6 +934,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   fp.group_mult = ix->group_mult.as<uint32_t>();
   fp.group_minid = ix->group_minid.as<int32_t>();
   fp.unit_thr = w.unit_thr;
+  fp.qthr = w.qthr;
   fp.out_dist = dist; fp.out_ids = ids;
   // register fast path when groups are large (few candidates per query)
   fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
@@ -984,6 +995,8 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   sp.cand = w.cand;
   sp.cand_cnt = w.cand_cnt;
   sp.unit_thr = w.unit_thr;
+  sp.qthr = w.qthr;
+  cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, st), "qthr init");
   cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(ivf)");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
@@ -994,6 +1007,7 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   fp.group_mult = ix->group_mult.as<uint32_t>();
   fp.group_minid = ix->group_minid.as<int32_t>();
   fp.unit_thr = w.unit_thr;
+  fp.qthr = w.qthr;
   fp.out_dist = dist; fp.out_ids = ids;
   fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
   cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");

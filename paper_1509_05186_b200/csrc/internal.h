@@ -45,6 +45,7 @@ struct FinParams {
   const uint32_t* group_mult = nullptr;
   const int32_t* group_minid = nullptr;
   const float* unit_thr = nullptr;      // [n_units][32] or null
+  const unsigned* qthr = nullptr;       // [Q] final per-query thresholds (float bits) or null
   float* out_dist = nullptr;
   int32_t* out_ids = nullptr;
   // two-tier finalize: a register fast path for few candidates per query; the
@@ -93,6 +94,7 @@ struct ScanParams {
   uint2* cand = nullptr;              // [n_units][kWarps][32][B] (dist bits, group)
   int* cand_cnt = nullptr;            // [n_units][kWarps][32]
   float* unit_thr = nullptr;          // [n_units][32] final CTA threshold per lane
+  unsigned* qthr = nullptr;           // [Q] per-query threshold (float bits), shared by all units
   int vec4 = 1;                       // query/codebook rows 16-byte aligned
   int fuse_fin = 0;                   // S == 1: finalize this CTA's queries in the scan kernel
   FinParams fin;

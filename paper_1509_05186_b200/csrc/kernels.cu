@@ -667,6 +667,7 @@ struct EmitCtx {
   int role;           // 0: forest partial (tree t>=1), 1: tree-0 leaves are the groups, 2: forest tuples
   int t;              // tree index for role 0
   int unit, chunk;
+  int q;              // query of this lane (-1: idle lane)
   float* part;        // this unit's partials base
   TopkState ts;
 };
@@ -690,10 +691,19 @@ __device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, u
 
 struct CntThr { int cnt; float thr; };
 
+// Per-query thresholds shared by every unit (CTA) that scans the query --
+// leaf segments, IVF probes -- through global atomicMin on the float bits
+// (distances are >= 0, so the bit order is the value order).  Initialised to
+// 0x7f7f7f7f (~3.4e38) by a memset; kThrNone marks "no bound yet".
+constexpr float kThrNone = 1e38f;
+
 __device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr, int B, int k,
                                              const uint32_t* gmult, const int32_t* gminid) {
   const int lane = lane_id();
-  unsigned full = __ballot_sync(FULLMASK, cnt > B - 32);
+  // full buffers, and (once) buffers that first reach k candidates while the
+  // lane has no threshold yet: an early exact bound stops the flood of
+  // candidates that every fresh warp would otherwise emit
+  unsigned full = __ballot_sync(FULLMASK, cnt > B - 32 || (cnt >= k && !(thr < kThrNone)));
   while (full) {
     const int L = __ffs(full) - 1;
     full &= full - 1;
@@ -707,101 +717,159 @@ __device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr
 
 __device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
   const ScanParams& p = *e.p;
-  if (__any_sync(FULLMASK, e.ts.cnt > p.B - 32)) {
+  if (__any_sync(FULLMASK, e.ts.cnt > p.B - 32 || (e.ts.cnt >= p.k && !(e.ts.thr < kThrNone)))) {
     const CntThr r = maybe_refresh(e.ts.warp_buf, e.ts.cnt, e.ts.thr, p.B, p.k, p.group_mult, p.group_minid);
     e.ts.cnt = r.cnt;
     e.ts.thr = r.thr;
   }
 }
 
-// Distance-Context update over the levels p..MT-1 of one leaf (P:249 for the
-// internal levels, P:239-243 for the leaf and its postfix): ctx[l] =
-// ctx[l-1] + T[l][code byte l], summed left to right exactly like naive ADC.
-// All lookups of the leaf are issued before the (dependent) additions.
+// Leaf record: one uint4 = 8 half-words; half-word l is the
+// pre-swizzled byte offset of table entry (level l, k = code byte l) inside
+// that level's 32 KB shared-memory region, (k << 7) | ((k & 31) << 2), so a
+// lookup is one extract/XOR with the lane's offset and one LDS whose immediate
+// carries the level's region base.  Level 0 of an 8-level tree lives in TMEM:
+// its half-word is the column k (bits 0..7) with the LCP with the previous
+// leaf in bits 8..11; trees with MT < 8 keep the LCP in half-word 7.
+#ifndef ET_SCAN_VARIANT
+#define ET_SCAN_VARIANT 3
+#endif
+
+// The scan kernel has no static shared memory, so its dynamic shared memory
+// (the tables, at offset 0) starts at the fixed shared-window address
+// kDsmBase (after the 1 KB the system reserves); scan_kernel traps if not.
+constexpr uint32_t kDsmBase = 0x400;
+
+template <int MT>
+__device__ __forceinline__ uint32_t rec_lcp(const uint4& r) {
+  if constexpr (MT == 8) return (r.x >> 8) & 15u;
+  else return r.w >> 16;
+}
+
+// Distance-Context update of one leaf, branch-free.  v[l] holds the table
+// entry T[l][k_l] of the path's node at depth l.  A leaf whose LCP with its
+// predecessor is p shares the nodes at depths < p, whose entries are still in
+// v[0..p-1]; it looks up levels p..MT-1 only (predicated LDS: the internal
+// nodes entered at depths p..depth-1, its own K, and its
+// postfix).  The distance is then the left-to-right sum
+// ((v0 + v1) + v2) + ... -- the Distance Context ctx[l] = ctx[l-1] + T[l][k_l]
+// of P:238-252 recomputed in registers, bit-identical to naive ADC.
+template <int MT>
+__device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t pl, uint32_t lane4,
+                                         uint32_t tq) {
+  constexpr int lv0 = (MT == 8) ? 1 : 0;
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  if constexpr (lv0 == 1) {
+    if (pl == 0) {   // warp-uniform: a new first-level subtree (level 0 in TMEM)
+      uint32_t t0 = tmem_ld1(tq + (w[0] & 255u));
+      tmem_wait_ld(t0);
+      v[0] = __uint_as_float(t0);
+    }
+  }
+#pragma unroll
+  for (int l = lv0; l < MT; ++l) {
+    const uint32_t off = (l & 1) ? ((w[l >> 1] >> 16) ^ lane4) : ((w[l >> 1] & 0xffffu) ^ lane4);
+    const uint32_t addr = off + (kDsmBase + ((uint32_t)(l - lv0) << 15));
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.le.u32 q, %2, %3;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
+                 : "+f"(v[l]) : "r"(addr), "r"(pl), "r"((uint32_t)l));
+  }
+  float s = v[0];
+#pragma unroll
+  for (int l = 1; l < MT; ++l) s = s + v[l];
+  return s;
+}
+
+// Scan of leaves [a, b) of one tree by one warp, lane = query.  A leaf costs
+// (MT - LCP) shared-memory lookups, MT - 1 FADDs and no branches.
+// Records: ET_SCAN_VARIANT 2 = warp-uniform loads (one L1 wavefront) two
+// leaves ahead behind an L1 prefetch; 3 = one coalesced load per 32 leaves
+// (next batch in flight) and 4 shuffles per leaf.
 template <int MT, int ROLE>
 __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b,
                           const float* lut0g) {
+  (void)lut0g;
   const ScanParams& p = *e.p;
-  constexpr int lv0 = (MT == 8) ? 1 : 0;
   const int lane = lane_id();
-  const uint32_t tab_s = smem_u32(sm.tab);
   const uint32_t lane4 = (uint32_t)lane << 2;
   const uint32_t tq = tmem_lane_base(sm.tmem);
-  float ctx[MT];
-#pragma unroll
-  for (int l = 0; l < MT; ++l) ctx[l] = 0.f;
   const bool topk = p.mode == kModeTopk;
-  int batch = 0;
-  for (uint32_t base = a; base < b; base += 32, ++batch) {
-    const uint32_t idx = base + lane;
-    const bool in = idx < b;
-    const uint4 myrec = in ? __ldg(tr.rec + idx) : make_uint4(0u, 0u, 0u, 0u);
-    const uint32_t mylcp = in ? (uint32_t)__ldg(tr.lcp + idx) : 0u;
-    uint32_t aux0 = 0, aux1 = 0;   // role 1: multiplicity; role 2: tuple range
-    if (ROLE == 1 && topk && in) aux0 = __ldg(p.group_mult + idx);
-    if (ROLE == 2 && in) { aux0 = __ldg(p.t0_tup_off + idx); aux1 = __ldg(p.t0_tup_off + idx + 1); }
-    const int n = (int)min(32u, b - base);
-    for (int j = 0; j < n; ++j) {
-      uint32_t w4[4];
-      w4[0] = __shfl_sync(FULLMASK, myrec.x, j);
-      w4[1] = (MT > 2) ? __shfl_sync(FULLMASK, myrec.y, j) : 0u;
-      w4[2] = (MT > 4) ? __shfl_sync(FULLMASK, myrec.z, j) : 0u;
-      w4[3] = (MT > 6) ? __shfl_sync(FULLMASK, myrec.w, j) : 0u;
-      int pl = (int)__shfl_sync(FULLMASK, mylcp, j);
-      if (base + j == a) pl = 0;   // first leaf of this warp's range: rebuild the whole path
-      // Distance Context update, branch-free: s_l = (l >= p) ? s_{l-1} + T[l][k_l]
-      // : ctx[l] (ctx[l] of the shared prefix), ctx[l] = s_l.  The addition for
-      // l >= p is exactly ctx[l-1] + T[l][k_l] of P:249; for l < p the select
-      // keeps the prefix's value and the (unused) sum is discarded.
-      uint32_t v0t = 0;
-      if (lv0 > 0 && pl == 0) v0t = tmem_ld1(tq + (w4[0] & 0xffffu));   // level 0 from TMEM
-      float v[MT];
+  const uint4* rec = tr.rec;
+  float v[MT];
 #pragma unroll
-      for (int l = lv0; l < MT; ++l) {
-        const uint32_t w = (l & 1) ? (w4[l >> 1] >> 16) : (w4[l >> 1] & 0xffffu);
-        v[l] = lds_if_w(tab_s + (w ^ lane4) + ((uint32_t)(l - lv0) << 15), l >= pl);
-      }
-      if (lv0 > 0) {
-        if (pl == 0) tmem_wait_ld(v0t);
-        v[0] = __uint_as_float(v0t);
-      }
-      float sacc = 0.f;
-#pragma unroll
-      for (int l = 0; l < MT; ++l) {
-        const float t = sacc + v[l];
-        sacc = (l >= pl) ? t : ctx[l];
-        ctx[l] = sacc;
-      }
-      const float dist = ctx[MT - 1];
-      const uint32_t leaf = base + j;
-      if constexpr (ROLE == 0) {
-        e.part[(size_t)p.part_base[e.t] + (size_t)leaf * 32 + lane] = dist;
-      } else if constexpr (ROLE == 1) {
-        const uint32_t mult = __shfl_sync(FULLMASK, aux0, j);
-        emit_group(e, dist, leaf, mult);
+  for (int l = 0; l < MT; ++l) v[l] = 0.f;
+  auto leaf_body = [&](uint32_t leaf, const uint4& r) {
+    const uint32_t pl = (leaf == a) ? 0u : rec_lcp<MT>(r);        // range start: rebuild the path
+    const float dist = dc_leaf<MT>(v, r, pl, lane4, tq);
+    if constexpr (ROLE == 0) {
+      e.part[(size_t)p.part_base[e.t] + (size_t)leaf * 32 + lane] = dist;
+    } else if constexpr (ROLE == 1) {
+      if (p.mode == kModeFull) {
+        p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + leaf] = dist;   // query-major rows
       } else {
-        const uint32_t t0 = __shfl_sync(FULLMASK, aux0, j);
-        const uint32_t t1 = __shfl_sync(FULLMASK, aux1, j);
-        for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
-          if (topk && ((g - t0) & 31) == 31) refresh_if_needed(e);
-          float dd = dist;
-          for (int tt = 1; tt < p.T; ++tt) {
-            const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
-            dd = dd + e.part[(size_t)p.part_base[tt] + (size_t)lf * 32 + lane];
-          }
-          const uint32_t mult = topk ? __ldg(p.group_mult + g) : 0u;
-          emit_group(e, dd, g, mult);
+        TopkState& ts = e.ts;
+        if (ts.active && dist <= ts.thr) {
+          ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), leaf);
+          ++ts.cnt;
+          if (__ldg(p.group_mult + leaf) >= (uint32_t)p.k) ts.thr = dist;   // one group bounds the k-th distance
         }
       }
-    }
-    if (topk && ROLE != 0) {   // prune full buffers; share the threshold with the CTA's other warps
-      refresh_if_needed(e);
-      if (e.ts.active) {
-        atomicMin(&sm.thr[lane], __float_as_uint(e.ts.thr));
-        e.ts.thr = __uint_as_float(*((volatile unsigned*)&sm.thr[lane]));
+    } else {
+      const uint32_t t0 = __ldg(p.t0_tup_off + leaf);
+      const uint32_t t1 = __ldg(p.t0_tup_off + leaf + 1);
+      for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
+        if (topk && ((g - t0) & 31) == 31) refresh_if_needed(e);
+        float dd = dist;
+        for (int tt = 1; tt < p.T; ++tt) {
+          const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
+          dd = dd + e.part[(size_t)p.part_base[tt] + (size_t)lf * 32 + lane];
+        }
+        const uint32_t mult = topk ? __ldg(p.group_mult + g) : 0u;
+        emit_group(e, dd, g, mult);
       }
     }
+  };
+  auto batch_end = [&]() {
+    if (topk && ROLE != 0) {   // prune full buffers; share the threshold with the CTA's other warps
+      refresh_if_needed(e);    // and with every other unit scanning the same query
+      if (e.ts.active) {
+        const unsigned mine = __float_as_uint(e.ts.thr);
+        atomicMin(&sm.thr[lane], mine);
+        unsigned t = *((volatile unsigned*)&sm.thr[lane]);
+        if (p.qthr) t = min(t, atomicMin(p.qthr + e.q, t));
+        e.ts.thr = __uint_as_float(t);
+      }
+    }
+  };
+#if ET_SCAN_VARIANT == 3
+  uint4 nxt = (a + lane < b) ? __ldg(rec + a + lane) : make_uint4(0u, 0u, 0u, 0u);
+  for (uint32_t base = a; base < b; base += 32) {
+    const uint4 mine = nxt;
+    const uint32_t nb = base + 32 + lane;
+    nxt = (nb < b) ? __ldg(rec + nb) : make_uint4(0u, 0u, 0u, 0u);   // next batch in flight
+    const int n = (int)min(32u, b - base);
+    for (int j = 0; j < n; ++j) {
+      uint4 r;
+      r.x = __shfl_sync(FULLMASK, mine.x, j);
+      r.y = (MT > 2) ? __shfl_sync(FULLMASK, mine.y, j) : 0u;
+      r.z = (MT > 4) ? __shfl_sync(FULLMASK, mine.z, j) : 0u;
+      r.w = __shfl_sync(FULLMASK, mine.w, j);   // levels 6-7, or the LCP when MT < 8
+      leaf_body(base + j, r);
+    }
+    batch_end();
   }
+#else
+  uint4 r0 = __ldg(rec + a);
+  uint4 r1 = (a + 1 < b) ? __ldg(rec + a + 1) : make_uint4(0u, 0u, 0u, 0u);
+  for (uint32_t leaf = a; leaf < b; ++leaf) {
+    if (((leaf - a) & 7u) == 0 && leaf + 16 < b)                     // keep L1 ahead of the loads
+      asm volatile("prefetch.global.L1 [%0];" :: "l"(rec + leaf + 16));
+    const uint4 r = r0;
+    r0 = r1;
+    r1 = (leaf + 2 < b) ? __ldg(rec + leaf + 2) : make_uint4(0u, 0u, 0u, 0u);
+    leaf_body(leaf, r);
+    if (((leaf - a) & 31u) == 31u || leaf + 1 == b) batch_end();
+  }
+#endif
 }
 
 template <int ROLE>
@@ -838,6 +906,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   const int chunk = unit / p.S;
   const int seg = unit - chunk * p.S;
   const int lane = lane_id(), warp = warp_id();
+  if (threadIdx.x == 0 && smem_u32(smem_raw) != kDsmBase) __trap();   // tab_ld's fixed base
   if (p.n_chunks_dev && chunk >= *p.n_chunks_dev) return;   // IVF: fewer chunks than the bound
   int MTmax = 0;
   for (int t = 0; t < p.T; ++t) MTmax = max(MTmax, p.tree[t].MT);
@@ -884,6 +953,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   e.p = &p;
   e.unit = unit;
   e.chunk = chunk;
+  e.q = sm.qidx[lane];
   e.part = p.partials ? p.partials + (size_t)unit * p.part_stride : nullptr;
   e.ts.active = lane < nq;
   e.ts.thr = e.ts.active ? __int_as_float(0x7f800000) : -1.0f;
@@ -958,7 +1028,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       }
       const int total = __shfl_sync(FULLMASK, inc, 31);
       const int excl = inc - myc;
-      const uint32_t tb = sm.thr[L];
+      uint32_t tb = sm.thr[L];
+      if (p.qthr && sm.qidx[L] >= 0) tb = min(tb, *((volatile unsigned*)(p.qthr + sm.qidx[L])));
       uint2* base = p.cand + ((size_t)unit * 32 + L) * kWarps * p.B;
       int n = 0;
       for (int i0 = 0; i0 < total; i0 += 32) {
@@ -1135,7 +1206,9 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
 
   // 1. threshold prefilter: min over the query's units of their final thresholds
   float thr = __int_as_float(0x7f800000);
-  if (unit_thr) {
+  if (p.qthr) {   // every unit of the query folded its final threshold into qthr
+    thr = __uint_as_float(__ldg(p.qthr + q));
+  } else if (unit_thr) {
     for (int j = s0; j < s1; ++j) {
       const int slot = fin_slot(p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
@@ -1508,7 +1581,9 @@ __global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __
 
   // 1. threshold prefilter (as the slow path)
   float thr = __int_as_float(0x7f800000);
-  if (p.unit_thr) {
+  if (p.qthr) {
+    thr = __uint_as_float(__ldg(p.qthr + q));
+  } else if (p.unit_thr) {
     for (int j = s0; j < s1; ++j) {
       const int slot = fin_slot(p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
