@@ -281,8 +281,8 @@ static void upload_groups(et_index* ix, const Groups& g, const std::vector<uint3
 // (l, k = code byte l) inside that level's 32 KB shared-memory table,
 // (k << 7) | ((k & 31) << 2), so a lookup is one XOR with the lane's offset.
 // Level 0 of an 8-level tree (held in TMEM) stores the column k with the LCP
-// with the previous leaf in bits 8..11; shorter trees keep the LCP in
-// half-word 7.
+// with the previous leaf in bits 8..11 and floor(log2(multiplicity)) in bits
+// 12..15; shorter trees keep both in half-word 7 (bits 0..3, 4..7).
 static std::vector<uint4> make_records(const HostTree& h) {
   const int MT = h.MT;
   std::vector<uint4> rec(h.code.size());
@@ -293,8 +293,11 @@ static std::vector<uint4> make_records(const HostTree& h) {
       w[l] = (MT == 8 && l == 0) ? k : ((k << 7) | ((k & 31u) << 2));
     }
     const uint32_t lcp = (i < h.lcp.size()) ? h.lcp[i] : 0u;
-    if (MT == 8) w[0] |= lcp << 8;
-    else w[7] = lcp;
+    const uint64_t mu = (i < h.mult.size()) ? h.mult[i] : 1;
+    uint32_t mb = 0;   // floor(log2(multiplicity)), capped at 15
+    while (mb < 15 && (2ull << mb) <= mu) ++mb;
+    if (MT == 8) w[0] |= (lcp << 8) | (mb << 12);
+    else w[7] = lcp | (mb << 4);
     rec[i] = make_uint4(w[0] | (w[1] << 16), w[2] | (w[3] << 16), w[4] | (w[5] << 16), w[6] | (w[7] << 16));
   }
   return rec;
@@ -634,7 +637,7 @@ static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool 
     w.leafdist = c.take<float>((size_t)pl.n_chunks * ix->n_groups * 32);
   } else {
     w.cand = c.take<uint2>((size_t)pl.n_units * kWarps * 32 * pl.B);
-    w.cand_cnt = c.take<int>((size_t)pl.n_units * 32);
+    w.cand_cnt = c.take<int>((size_t)pl.n_units * 32 * kWarps);
     w.unit_thr = c.take<float>((size_t)pl.n_units * 32);
     w.qthr = c.take<unsigned>((size_t)Q);
   }
@@ -938,6 +941,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   fp.out_dist = dist; fp.out_ids = ids;
   // register fast path when groups are large (few candidates per query)
   fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
+  sp.compact = !fp.fast;
   if (false && pl.S == 1) {   // fused finalize (kept for experiments; the separate kernel hides latency better)
     sp.fuse_fin = 1;
     sp.fin = fp;
@@ -997,6 +1001,7 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   sp.unit_thr = w.unit_thr;
   sp.qthr = w.qthr;
   cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, st), "qthr init");
+  sp.compact = !((double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0));   // = !fp.fast
   cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(ivf)");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;

@@ -97,6 +97,7 @@ struct ScanParams {
   unsigned* qthr = nullptr;           // [Q] per-query threshold (float bits), shared by all units
   int vec4 = 1;                       // query/codebook rows 16-byte aligned
   int fuse_fin = 0;                   // S == 1: finalize this CTA's queries in the scan kernel
+  int compact = 0;                    // merge each lane's 16 per-warp lists at the end (long lists)
   FinParams fin;
 };
 

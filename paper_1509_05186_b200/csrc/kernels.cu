@@ -27,6 +27,20 @@ namespace et {
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 
+// Optional per-CTA phase timestamps (experiment builds: -DET_PHASE_TIMING).
+#ifdef ET_PHASE_TIMING
+__device__ unsigned long long g_phase[1 << 16][8];
+__device__ __forceinline__ void phase_mark(int unit, int i) {
+  if (threadIdx.x == 0 && unit < (1 << 16)) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_phase[unit][i] = t;
+  }
+}
+#else
+__device__ __forceinline__ void phase_mark(int, int) {}
+#endif
+
 // ---------------------------------------------------------------------------
 // table build helpers
 // ---------------------------------------------------------------------------
@@ -449,6 +463,7 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
   float cw[SS], cwn[SS];
   if (active) load_cw(0, cw);
   __syncthreads();                                   // stage complete
+  phase_mark(unit, 5);
   if constexpr (MT == 8) {
     // level 0 -> region of level 6 (free until level 6 is built) -> TMEM
     const uint32_t l0_s = tab_s + (5u << 15);
@@ -460,20 +475,24 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
     }
     __syncthreads();
     tmem_fence_after();
-    tmem_load_from_smem(sm, l0_s);
+    tmem_load_from_smem(sm, l0_s);   // overlaps the other warps' level-1.. builds
     tmem_fence_before();
-    __syncthreads();
+    phase_mark(unit, 6);
   }
   // levels lv0 .. MT-2 (their queries staged in the last level's region)
-  if (active) {
-    for (int l = lv0; l < MT - 1; ++l) {
-      if (l + 1 < MT) load_cw(l + 1, cwn);           // prefetch the next level's codeword
+  for (int l = lv0; l < MT - 1; ++l) {
+    // level 6 of an 8-level tree reuses level 0's staging region: every warp's
+    // TMEM copy must be done
+    if (MT == 8 && l == MT - 2) __syncthreads();
+    if (active) {
+      load_cw(l + 1, cwn);                           // prefetch the next level's codeword
       item(tab_s + ((uint32_t)(l - lv0) << 15), region_s + (uint32_t)(l * np) * pair_bytes, cw);
 #pragma unroll
       for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
     }
   }
   __syncthreads();                                   // region free: build the last level into it
+  phase_mark(unit, 7);
   if (active) item(region_s, stage_s, cw);
   __syncthreads();
   if constexpr (MT == 8) tmem_fence_after();         // TMEM level 0 visible to the scan's tcgen05.ld
@@ -730,7 +749,8 @@ __device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
 // lookup is one extract/XOR with the lane's offset and one LDS whose immediate
 // carries the level's region base.  Level 0 of an 8-level tree lives in TMEM:
 // its half-word is the column k (bits 0..7) with the LCP with the previous
-// leaf in bits 8..11; trees with MT < 8 keep the LCP in half-word 7.
+// leaf in bits 8..11 and floor(log2(multiplicity)) in bits 12..15; trees with
+// MT < 8 keep both in half-word 7 (bits 0..3, 4..7).
 #ifndef ET_SCAN_VARIANT
 #define ET_SCAN_VARIANT 3
 #endif
@@ -740,10 +760,18 @@ __device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
 // kDsmBase (after the 1 KB the system reserves); scan_kernel traps if not.
 constexpr uint32_t kDsmBase = 0x400;
 
+
 template <int MT>
 __device__ __forceinline__ uint32_t rec_lcp(const uint4& r) {
   if constexpr (MT == 8) return (r.x >> 8) & 15u;
-  else return r.w >> 16;
+  else return (r.w >> 16) & 15u;
+}
+// floor(log2(multiplicity)) of the leaf's group (single trees), capped at 15:
+// 2^bucket >= k proves the group alone holds k ids (a conservative test)
+template <int MT>
+__device__ __forceinline__ uint32_t rec_mbucket(const uint4& r) {
+  if constexpr (MT == 8) return (r.x >> 12) & 15u;
+  else return (r.w >> 20) & 15u;
 }
 
 // Distance-Context update of one leaf, branch-free.  v[l] holds the table
@@ -810,7 +838,7 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
         if (ts.active && dist <= ts.thr) {
           ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), leaf);
           ++ts.cnt;
-          if (__ldg(p.group_mult + leaf) >= (uint32_t)p.k) ts.thr = dist;   // one group bounds the k-th distance
+          if ((1u << rec_mbucket<MT>(r)) >= (uint32_t)p.k) ts.thr = dist;   // one group bounds the k-th distance
         }
       }
     } else {
@@ -907,6 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   const int seg = unit - chunk * p.S;
   const int lane = lane_id(), warp = warp_id();
   if (threadIdx.x == 0 && smem_u32(smem_raw) != kDsmBase) __trap();   // tab_ld's fixed base
+  phase_mark(unit, 0);
   if (p.n_chunks_dev && chunk >= *p.n_chunks_dev) return;   // IVF: fewer chunks than the bound
   int MTmax = 0;
   for (int t = 0; t < p.T; ++t) MTmax = max(MTmax, p.tree[t].MT);
@@ -973,7 +1002,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     bool level0_done = false;   // resident build copies level 0 to TMEM itself
     if constexpr (SS == kDC && MTC > 0) {
       if (p.luts) { build_tables<SS>(p, sm, t, unit, nq, cell); __syncthreads(); }
-      else { build_tables_resident<SS, MTC>(p, sm, t, unit, nq, cell); level0_done = true; }
+      else { phase_mark(unit, 1); build_tables_resident<SS, MTC>(p, sm, t, unit, nq, cell); level0_done = true; phase_mark(unit, 2); }
     } else {
       build_tables<SS>(p, sm, t, unit, nq, cell);
       __syncthreads();
@@ -1009,12 +1038,18 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     __syncthreads();   // partials visible / tables free for the next tree
     tmem_fence_after();
   }
+  phase_mark(unit, 3);
   if (use_tmem && warp == 0) tmem_dealloc(sm.tmem);
 
-  if (p.mode == kModeTopk) {
-    // Merge the 16 warps' candidates of each lane into one list under the CTA's
-    // final threshold, in place: lane L's buffers are contiguous, so the kept
-    // entries are compacted to the front (write position <= read position).
+  if (p.mode == kModeTopk && !p.compact) {
+    // per-warp candidate lists stay where the scan wrote them: lane L's 16
+    // buffers are contiguous, counts at cand_cnt[(unit*32 + L)*kWarps + warp]
+    p.cand_cnt[((size_t)unit * 32 + lane) * kWarps + warp] = e.ts.cnt;
+    if (warp == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + lane] = __uint_as_float(sm.thr[lane]);
+  } else if (p.mode == kModeTopk) {
+    // Long lists (small groups): merge the 16 warps' candidates of each lane
+    // into its first buffer under the final threshold, in place -- lane L's
+    // buffers are contiguous, so write position <= read position.
     int* cnt_s = reinterpret_cast<int*>(smem_raw);   // tables are dead now
     cnt_s[warp * 32 + lane] = e.ts.cnt;
     __syncthreads();
@@ -1049,10 +1084,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
         if (keep) base[n + __popc(m & ((1u << lane) - 1u))] = v;
         n += __popc(m);
       }
-      if (lane == 0) {
-        p.cand_cnt[(size_t)unit * 32 + L] = n;
-        if (p.unit_thr) p.unit_thr[(size_t)unit * 32 + L] = __uint_as_float(tb);
-      }
+      if (lane < kWarps) p.cand_cnt[((size_t)unit * 32 + L) * kWarps + lane] = (lane == 0) ? n : 0;
+      if (lane == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + L] = __uint_as_float(tb);
     }
     if (p.fuse_fin) {
       __syncthreads();
@@ -1060,6 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       for (int i = warp; i < nq; i += kWarps) finalize_query(p.fin, *fw, sm.qidx[i]);
     }
   }
+  phase_mark(unit, 4);
 }
 
 size_t scan_smem_bytes(int MTmax) {
@@ -1159,6 +1193,17 @@ __device__ __forceinline__ int fin_slot(const FinParams& p, int64_t q, int j) {
   return __ldg(p.qslot + j);
 }
 
+// Candidate list li of query q, 0 <= li < (s1 - s0) * S * kWarps: one per
+// (slot, leaf segment, scan warp).  Its count is cand_cnt[list], its entries
+// cand[list * B ...] (the scan kernel's per-warp, per-lane buffers).
+__device__ __forceinline__ size_t fin_list(const FinParams& p, int64_t q, int s0, int li) {
+  const int per = p.S * kWarps;
+  const int j = li / per, r = li - j * per;
+  const int sg = r / kWarps, w = r - sg * kWarps;
+  const int slot = fin_slot(p, q, s0 + j);
+  return ((size_t)((slot >> 5) * p.S + sg) * 32 + (slot & 31)) * kWarps + w;
+}
+
 // Enumerates the candidates of query q: smem copy when they fit, else global.
 // f(key, group, multiplicity) is called once per candidate by the owning lane.
 // Each (slot, segment) unit list holds cand_cnt[unit*32+lane] entries at
@@ -1181,17 +1226,14 @@ struct CandSrc {
       return;
     }
     const uint32_t tb = __float_as_uint(thr);
-    for (int j = s0; j < s1; ++j) {
-      const int slot = fin_slot(*p, q, j);
-      const int chunk = slot >> 5, ln = slot & 31;
-      for (int sg = 0; sg < p->S; ++sg) {
-        const size_t ul = (size_t)(chunk * p->S + sg) * 32 + ln;
-        const int c = __ldg(p->cand_cnt + ul);
-        const uint2* eb = p->cand + ul * kWarps * p->B;
-        for (int i = lane; i < c; i += 32) {
-          const uint2 v = eb[i];
-          if (v.x <= tb) f(v.x, v.y, __ldg(p->group_mult + v.y));
-        }
+    const int nl = (s1 - s0) * p->S * kWarps;
+    for (int li = 0; li < nl; ++li) {
+      const size_t ul = fin_list(*p, q, s0, li);
+      const int c = __ldg(p->cand_cnt + ul);
+      const uint2* eb = p->cand + ul * p->B;
+      for (int i = lane; i < c; i += 32) {
+        const uint2 v = eb[i];
+        if (v.x <= tb) f(v.x, v.y, __ldg(p->group_mult + v.y));
       }
     }
   }
@@ -1227,14 +1269,13 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
     uint32_t* K_ = fw.key;
     uint32_t* G_ = fw.grp;
     uint32_t* U_ = fw.mul;
-    const int nl = (s1 - s0) * p.S;
+    const int nl = (s1 - s0) * p.S * kWarps;
     for (int l0 = 0; l0 < nl && !overflow; l0 += 32) {
       const int li = l0 + lane;
       size_t ul = 0;
       int myc = 0;
       if (li < nl) {
-        const int slot = fin_slot(p, q, s0 + li / p.S);
-        ul = (size_t)((slot >> 5) * p.S + li % p.S) * 32 + (slot & 31);
+        ul = fin_list(p, q, s0, li);
         myc = __ldg(p.cand_cnt + ul);
       }
       int inc = myc;
@@ -1256,7 +1297,7 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
         const int wo = __shfl_sync(FULLMASK, excl, w);
         const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
         uint2 v = make_uint2(0xffffffffu, 0);
-        if (idx < total) v = p.cand[ulw * kWarps * p.B + (idx - wo)];
+        if (idx < total) v = p.cand[ulw * p.B + (idx - wo)];
         const bool keep = (idx < total) && v.x <= tb;
         const unsigned m = __ballot_sync(FULLMASK, keep);
         const int pos = n + __popc(m & ((1u << lane) - 1u));
@@ -1598,14 +1639,13 @@ __global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __
   uint2 r0 = make_uint2(0xffffffffu, 0), r1 = make_uint2(0xffffffffu, 0);
   int n = 0;
   bool overflow = false;
-  const int nl = (s1 - s0) * p.S;
+  const int nl = (s1 - s0) * p.S * kWarps;
   for (int l0 = 0; l0 < nl && !overflow; l0 += 32) {
     const int li = l0 + lane;
     size_t ul = 0;
     int myc = 0;
     if (li < nl) {
-      const int slot = fin_slot(p, q, s0 + li / p.S);
-      ul = (size_t)((slot >> 5) * p.S + li % p.S) * 32 + (slot & 31);
+      ul = fin_list(p, q, s0, li);
       myc = __ldg(p.cand_cnt + ul);
     }
     int inc = myc;
@@ -1627,7 +1667,7 @@ __global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __
       const int wo = __shfl_sync(FULLMASK, excl, w);
       const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
       uint2 v = make_uint2(0xffffffffu, 0);
-      if (idx < total) v = p.cand[ulw * kWarps * p.B + (idx - wo)];
+      if (idx < total) v = p.cand[ulw * p.B + (idx - wo)];
       const bool keep = (idx < total) && v.x <= tb;
       const unsigned m = __ballot_sync(FULLMASK, keep);
       const int c = __popc(m);
@@ -2166,3 +2206,10 @@ cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist
 }
 
 }  // namespace et
+
+#ifdef ET_PHASE_TIMING
+extern "C" int et_debug_phases(unsigned long long* out, int n_units) {
+  if (n_units > (1 << 16)) n_units = 1 << 16;
+  return (int)cudaMemcpyFromSymbol(out, et::g_phase, (size_t)n_units * 8 * sizeof(unsigned long long));
+}
+#endif

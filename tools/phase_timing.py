@@ -1,0 +1,54 @@
+"""Per-CTA phase durations of the scan kernel (experiment build with -DET_PHASE_TIMING).
+
+  python tools/phase_timing.py --config c2
+Phases: 0 start, 1 build start, 5 staged, 6 level 0 in TMEM, 7 levels 1..MT-2 built,
+2 build done, 3 scan done, 4 compaction done.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+LIB = os.path.join(ROOT, "paper_1509_05186_b200", "_build", "phase", "libetree.so")
+os.environ["ET_LIB_PATH"] = LIB
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    a = ap.parse_args()
+    import torch
+    from paper_1509_05186_b200 import api
+    cfg = bench.workload_config(a.config)
+    dev = torch.device("cuda", 0)
+    st = bench.prepare_ours(cfg, dev, 0, 1)
+    ix = st["ix"]
+    for _ in range(3):
+        ix.et_etree_topk(cfg.topk, queries=st["q_dev"], codebooks=st["cb_dev"])
+    torch.cuda.synchronize()
+    lib = api._lib.load()
+    n = 1 << 16
+    buf = np.zeros((n, 8), dtype=np.uint64)
+    lib.et_debug_phases.argtypes = [C.c_void_p, C.c_int]
+    lib.et_debug_phases(buf.ctypes.data, n)
+    used = buf[:, 0] > 0
+    b = buf[used].astype(np.float64)
+    t0 = b[:, 0].min()
+    order = [(0, 1, "start->build"), (1, 5, "stage"), (5, 6, "level0+TMEM"), (6, 7, "levels 1..6"),
+             (7, 2, "last level"), (2, 3, "scan"), (3, 4, "compaction")]
+    print(f"units {used.sum()}  kernel span {(b[:, 4].max() - t0) / 1e3:.1f} us")
+    for i, j, name in order:
+        d = (b[:, j] - b[:, i]) / 1e3
+        print(f"{name:14s} mean {d.mean():7.2f} us  p50 {np.median(d):7.2f}  max {d.max():7.2f}")
+    tot = (b[:, 4] - b[:, 0]) / 1e3
+    print(f"{'total/CTA':14s} mean {tot.mean():7.2f} us")
+
+
+if __name__ == "__main__":
+    main()
