@@ -927,6 +927,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   sp.cand_cnt = w.cand_cnt;
   sp.unit_thr = w.unit_thr;
   sp.qthr = w.qthr;
+  sp.qthr_shared = pl.S > 1;
   cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, (cudaStream_t)stream), "qthr init");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
@@ -1000,6 +1001,7 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   sp.cand_cnt = w.cand_cnt;
   sp.unit_thr = w.unit_thr;
   sp.qthr = w.qthr;
+  sp.qthr_shared = 1;
   cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, st), "qthr init");
   sp.compact = !((double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0));   // = !fp.fast
   cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(ivf)");

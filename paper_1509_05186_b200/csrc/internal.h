@@ -95,6 +95,7 @@ struct ScanParams {
   int* cand_cnt = nullptr;            // [n_units][kWarps][32]
   float* unit_thr = nullptr;          // [n_units][32] final CTA threshold per lane
   unsigned* qthr = nullptr;           // [Q] per-query threshold (float bits), shared by all units
+  int qthr_shared = 0;                // several units per query (S > 1, IVF): share during the scan
   int vec4 = 1;                       // query/codebook rows 16-byte aligned
   int fuse_fin = 0;                   // S == 1: finalize this CTA's queries in the scan kernel
   int compact = 0;                    // merge each lane's 16 per-warp lists at the end (long lists)

@@ -59,6 +59,9 @@ extern __shared__ __align__(16) unsigned char et_dsm[];
 __device__ __forceinline__ float4 lds4_off(uint32_t off) {
   return *reinterpret_cast<const float4*>(et_dsm + off);
 }
+__device__ __forceinline__ void sts_off(uint32_t off, float v) {
+  *reinterpret_cast<float*>(et_dsm + off) = v;
+}
 
 // Explicit shared-memory accesses (32-bit shared addresses; avoids generic
 // addressing in the hot loops).
@@ -358,6 +361,40 @@ __device__ __forceinline__ void tmem_load_from_smem(const SmemScan& sm, uint32_t
   tmem_wait_st();
 }
 
+// Staging layout of the resident build: level l's query pairs at
+// region + l * kStageLevelBytes (16 pairs x 16 dims x 2 queries), the last
+// level's in the small stage.  Element (slot i, dim j) of a level lives at
+// (i / 2) * 128 + j * 8 + (i % 2) * 4.
+constexpr uint32_t kStageLevelBytes = 16 * 16 * 2 * 4;
+
+// Issued at kernel entry (plain E-Tree tables, no coarse residual): the
+// chunk's query sub-vectors are copied straight into the staging layout with
+// cp.async (no registers held), overlapping the CTA's setup (TMEM allocation,
+// first barrier); the build waits with cp.async.wait_all.  Slots without a
+// query are left unwritten (their entries are never looked up).
+template <int SS, int MT>
+__device__ __forceinline__ void stage_async(const ScanParams& p, int t, int chunk, int nch, uint32_t region_s,
+                                            uint32_t stage_s) {
+  const TreeDev& tr = p.tree[t];
+  const int i = threadIdx.x >> 4, j = threadIdx.x & (SS - 1);
+  int q = -1;
+  if (p.flatQ > 0) {
+    const int64_t s0 = (int64_t)chunk * p.flatQ / nch, s1 = (int64_t)(chunk + 1) * p.flatQ / nch;
+    q = (s0 + i < s1) ? (int)(s0 + i) : -1;
+  } else {
+    q = __ldg(p.chunk_q + (size_t)chunk * 32 + i);
+  }
+  if (q < 0) return;
+  const float* xr = p.queries + (size_t)q * p.d + j;
+  const uint32_t o = (uint32_t)(i >> 1) * 128u + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
+#pragma unroll
+  for (int l = 0; l < MT; ++l) {
+    const uint32_t dst = (l < MT - 1) ? region_s + (uint32_t)l * kStageLevelBytes + o : stage_s + o;
+    const float* src = xr + (size_t)p.layer_sub[tr.layer0 + l] * SS;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+  }
+}
+
 // Resident-staging table build for s == 16 (every d = 128 configuration).
 // The active queries' sub-vectors are staged ONCE, as query pairs
 // [level][pair][dim][2], levels 0..MT-2 into the shared-memory region of the
@@ -368,8 +405,8 @@ __device__ __forceinline__ void tmem_load_from_smem(const SmemScan& sm, uint32_t
 // broadcast LDS.128 loads of the staged pairs.  With 8 levels, level 0 is
 // built first into the region of level 6 and copied to TMEM.
 template <int SS, int MT>
-__device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq,
-                                      int cell) {
+__device__ __forceinline__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, int t, int unit,
+                                                      int nq, int cell, bool staged) {
   static_assert(SS == kDC, "resident staging handles s == 16");
   const TreeDev& tr = p.tree[t];
   constexpr int lv0 = (MT == 8) ? 1 : 0;   // level 0 of an 8-level tree lives in TMEM
@@ -380,30 +417,26 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
   const uint32_t stage_s = smem_u32(sm.stage);
   const int np = (nq + 1) >> 1;                                          // query pairs
   const uint32_t pair_bytes = SS * 2 * 4;                                // 128 B per (level, pair)
-  __syncthreads();                                   // previous tree's scan is done with the tables
-  {
-    // thread -> (query slot i, dim j); all loads first, then the stores.  The
-    // odd partner of an odd nq is staged as 0 (its entries are never stored).
+  if (staged) {
+    asm volatile("cp.async.wait_all;" ::: "memory");   // this thread's stage_async copies landed
+  } else {
+    __syncthreads();                                 // previous tree's scan is done with the tables
+    // thread -> (query slot i, dim j); all loads first, then the stores
     const int i = threadIdx.x >> 4, j = threadIdx.x & (SS - 1);
-    if (i < nq + (nq & 1)) {
+    if (i < nq) {
       float v[MT];
-      if (i < nq) {
-        const int q = sm.qidx[i];
-        const float* xr = p.queries + (size_t)q * d + j;
-        const float* cr = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + j : nullptr;
+      const int q = sm.qidx[i];
+      const float* xr = p.queries + (size_t)q * d + j;
+      const float* cr = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + j : nullptr;
 #pragma unroll
-        for (int l = 0; l < MT; ++l) v[l] = __ldg(xr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
-        if (cr) {
+      for (int l = 0; l < MT; ++l) v[l] = __ldg(xr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
+      if (cr) {
 #pragma unroll
-          for (int l = 0; l < MT; ++l) v[l] -= __ldg(cr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
-        }
-      } else {
-#pragma unroll
-        for (int l = 0; l < MT; ++l) v[l] = 0.f;
+        for (int l = 0; l < MT; ++l) v[l] -= __ldg(cr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
       }
       const uint32_t o = (uint32_t)(i >> 1) * pair_bytes + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
 #pragma unroll
-      for (int l = 0; l < MT - 1; ++l) sts(region_s + (uint32_t)(l * np) * pair_bytes + o, v[l]);
+      for (int l = 0; l < MT - 1; ++l) sts(region_s + (uint32_t)l * kStageLevelBytes + o, v[l]);
       sts(stage_s + o, v[MT - 1]);
     }
   }
@@ -412,29 +445,31 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
   const bool kvalid = k < K;
   const int p0 = g ? (np + 1) >> 1 : 0, p1 = g ? np : (np + 1) >> 1;
   const bool active = kb * 32 < K;                   // K < 256: idle codeword blocks
+  const uint32_t dsm_s = smem_u32(et_dsm);
   auto load_cw = [&](int l, float (&c)[SS]) {
     const int m = p.layer_sub[tr.layer0 + l];
     const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
 #pragma unroll
     for (int j = 0; j < SS; j += 4) {
-      const float4 v = kvalid ? __ldg(reinterpret_cast<const float4*>(crow + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v = __ldg(reinterpret_cast<const float4*>(crow + j));
       c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
     }
   };
-  // entries of level-slot `dst` (table region index) for pairs [p0, p1) of stage xs
+  // Entries of one table (region dst_s) for this warp's query pairs [p0, p1)
+  // of stage xs_s, two pairs (four entries) per iteration.  Every lane writes
+  // all query slots of its codeword's row: slots >= nq are never looked up
+  // (and rows k >= K never addressed), so no store is predicated.
   auto item = [&](uint32_t dst_s, uint32_t xs_s, const float (&c)[SS]) {
-    const uint32_t lane4 = (uint32_t)lane << 2;
-    auto put = [&](int i, float a) {
-      if (kvalid && i < nq) sts(tab_addr(dst_s, 0, (uint32_t)k, (uint32_t)i << 2), a);
-    };
-    (void)lane4;
+    const uint32_t drow = dst_s - dsm_s + ((uint32_t)k << 7);   // this lane's row (byte offset)
+    const uint32_t kk = (uint32_t)k << 2;
+    uint32_t xo = xs_s - dsm_s + (uint32_t)p0 * pair_bytes;
+    uint32_t i4 = (uint32_t)p0 << 3;                             // 4 * (first query of the pair)
     int pi = p0;
-    for (; pi + 1 < p1; pi += 2) {
-      const uint32_t x0 = xs_s + (uint32_t)pi * pair_bytes, x1 = x0 + pair_bytes;
+    for (; pi + 1 < p1; pi += 2, xo += 2 * pair_bytes, i4 += 16) {
       unsigned long long a0 = 0ull, a1 = 0ull;
 #pragma unroll
       for (int j = 0; j < SS; j += 2) {
-        const float4 u0 = lds4(x0 + (uint32_t)j * 8u), u1 = lds4(x1 + (uint32_t)j * 8u);
+        const float4 u0 = lds4_off(xo + (uint32_t)j * 8u), u1 = lds4_off(xo + pair_bytes + (uint32_t)j * 8u);
         const unsigned long long cj = f2pack(c[j], c[j]), cj1 = f2pack(c[j + 1], c[j + 1]);
         unsigned long long t0 = f2sub(f2pack(u0.x, u0.y), cj), t1 = f2sub(f2pack(u1.x, u1.y), cj);
         a0 = f2sqacc(t0, a0); a1 = f2sqacc(t1, a1);
@@ -444,20 +479,23 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
       float e0, o0, e1, o1;
       f2unpack(a0, e0, o0);
       f2unpack(a1, e1, o1);
-      put(2 * pi, e0); put(2 * pi + 1, o0); put(2 * pi + 2, e1); put(2 * pi + 3, o1);
+      sts_off(drow + ((i4 ^ kk) & 0x7cu), e0);
+      sts_off(drow + (((i4 + 4) ^ kk) & 0x7cu), o0);
+      sts_off(drow + (((i4 + 8) ^ kk) & 0x7cu), e1);
+      sts_off(drow + (((i4 + 12) ^ kk) & 0x7cu), o1);
     }
     if (pi < p1) {
-      const uint32_t x0 = xs_s + (uint32_t)pi * pair_bytes;
       unsigned long long a0 = 0ull;
 #pragma unroll
       for (int j = 0; j < SS; j += 2) {
-        const float4 u0 = lds4(x0 + (uint32_t)j * 8u);
+        const float4 u0 = lds4_off(xo + (uint32_t)j * 8u);
         a0 = f2sqacc(f2sub(f2pack(u0.x, u0.y), f2pack(c[j], c[j])), a0);
         a0 = f2sqacc(f2sub(f2pack(u0.z, u0.w), f2pack(c[j + 1], c[j + 1])), a0);
       }
       float e0, o0;
       f2unpack(a0, e0, o0);
-      put(2 * pi, e0); put(2 * pi + 1, o0);
+      sts_off(drow + ((i4 ^ kk) & 0x7cu), e0);
+      sts_off(drow + (((i4 + 4) ^ kk) & 0x7cu), o0);
     }
   };
   float cw[SS], cwn[SS];
@@ -486,7 +524,7 @@ __device__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, i
     if (MT == 8 && l == MT - 2) __syncthreads();
     if (active) {
       load_cw(l + 1, cwn);                           // prefetch the next level's codeword
-      item(tab_s + ((uint32_t)(l - lv0) << 15), region_s + (uint32_t)(l * np) * pair_bytes, cw);
+      item(tab_s + ((uint32_t)(l - lv0) << 15), region_s + (uint32_t)l * kStageLevelBytes, cw);
 #pragma unroll
       for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
     }
@@ -693,7 +731,8 @@ struct EmitCtx {
 
 // Append one group's distance to this lane's candidates if it can still be in
 // the top-k (hot path: no calls, no syncs).  Buffers are pruned at batch
-// boundaries by maybe_refresh, which keeps >= 32 free slots per lane.
+// boundaries by maybe_refresh, which keeps >= 64 free slots per lane (a batch
+// of 32 leaves of each of a warp's two streams).
 __device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, uint32_t mult) {
   const ScanParams& p = *e.p;
   if (p.mode == kModeFull) {
@@ -722,7 +761,7 @@ __device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr
   // full buffers, and (once) buffers that first reach k candidates while the
   // lane has no threshold yet: an early exact bound stops the flood of
   // candidates that every fresh warp would otherwise emit
-  unsigned full = __ballot_sync(FULLMASK, cnt > B - 32 || (cnt >= k && !(thr < kThrNone)));
+  unsigned full = __ballot_sync(FULLMASK, cnt > B - 64 || (cnt >= k && !(thr < kThrNone)));
   while (full) {
     const int L = __ffs(full) - 1;
     full &= full - 1;
@@ -736,7 +775,7 @@ __device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr
 
 __device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
   const ScanParams& p = *e.p;
-  if (__any_sync(FULLMASK, e.ts.cnt > p.B - 32 || (e.ts.cnt >= p.k && !(e.ts.thr < kThrNone)))) {
+  if (__any_sync(FULLMASK, e.ts.cnt > p.B - 64 || (e.ts.cnt >= p.k && !(e.ts.thr < kThrNone)))) {
     const CntThr r = maybe_refresh(e.ts.warp_buf, e.ts.cnt, e.ts.thr, p.B, p.k, p.group_mult, p.group_minid);
     e.ts.cnt = r.cnt;
     e.ts.thr = r.thr;
@@ -782,24 +821,28 @@ __device__ __forceinline__ uint32_t rec_mbucket(const uint4& r) {
 // postfix).  The distance is then the left-to-right sum
 // ((v0 + v1) + v2) + ... -- the Distance Context ctx[l] = ctx[l-1] + T[l][k_l]
 // of P:238-252 recomputed in registers, bit-identical to naive ADC.
+// `valid` = false makes the call a no-op on v (the padding leaf of a stream).
 template <int MT>
-__device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t pl, uint32_t lane4,
-                                         uint32_t tq) {
+__device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t pl, bool valid,
+                                         uint32_t lane4, uint32_t tq) {
   constexpr int lv0 = (MT == 8) ? 1 : 0;
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  const uint32_t plv = valid ? pl : 255u;   // 255: no level is looked up
   if constexpr (lv0 == 1) {
-    if (pl == 0) {   // warp-uniform: a new first-level subtree (level 0 in TMEM)
-      uint32_t t0 = tmem_ld1(tq + (w[0] & 255u));
-      tmem_wait_ld(t0);
-      v[0] = __uint_as_float(t0);
-    }
+    // level 0 (TMEM) only on a new first-level subtree: a warp-uniform predicate
+    uint32_t t0 = __float_as_uint(v[0]);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.u32 q, %2, 0;\n\t"
+                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
+                 : "+r"(t0) : "r"(tq + (w[0] & 255u)), "r"(plv));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0));
+    v[0] = __uint_as_float(t0);
   }
 #pragma unroll
   for (int l = lv0; l < MT; ++l) {
     const uint32_t off = (l & 1) ? ((w[l >> 1] >> 16) ^ lane4) : ((w[l >> 1] & 0xffffu) ^ lane4);
     const uint32_t addr = off + (kDsmBase + ((uint32_t)(l - lv0) << 15));
     asm volatile("{\n\t.reg .pred q;\n\tsetp.le.u32 q, %2, %3;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
-                 : "+f"(v[l]) : "r"(addr), "r"(pl), "r"((uint32_t)l));
+                 : "+f"(v[l]) : "r"(addr), "r"(plv), "r"((uint32_t)l));
   }
   float s = v[0];
 #pragma unroll
@@ -807,11 +850,11 @@ __device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_
   return s;
 }
 
-// Scan of leaves [a, b) of one tree by one warp, lane = query.  A leaf costs
+// Scan of leaves [a, b) of one tree by one warp, lane = query.  The range is
+// split into two halves scanned in lockstep (two independent dependency
+// chains per warp); records come with one coalesced load per 32 leaves per
+// half (the next batch in flight) and four shuffles per leaf.  A leaf costs
 // (MT - LCP) shared-memory lookups, MT - 1 FADDs and no branches.
-// Records: ET_SCAN_VARIANT 2 = warp-uniform loads (one L1 wavefront) two
-// leaves ahead behind an L1 prefetch; 3 = one coalesced load per 32 leaves
-// (next batch in flight) and 4 shuffles per leaf.
 template <int MT, int ROLE>
 __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b,
                           const float* lut0g) {
@@ -822,39 +865,16 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
   const uint32_t tq = tmem_lane_base(sm.tmem);
   const bool topk = p.mode == kModeTopk;
   const uint4* rec = tr.rec;
-  float v[MT];
-#pragma unroll
-  for (int l = 0; l < MT; ++l) v[l] = 0.f;
-  auto leaf_body = [&](uint32_t leaf, const uint4& r) {
-    const uint32_t pl = (leaf == a) ? 0u : rec_lcp<MT>(r);        // range start: rebuild the path
-    const float dist = dc_leaf<MT>(v, r, pl, lane4, tq);
-    if constexpr (ROLE == 0) {
-      e.part[(size_t)p.part_base[e.t] + (size_t)leaf * 32 + lane] = dist;
-    } else if constexpr (ROLE == 1) {
-      if (p.mode == kModeFull) {
-        p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + leaf] = dist;   // query-major rows
-      } else {
-        TopkState& ts = e.ts;
-        if (ts.active && dist <= ts.thr) {
-          ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), leaf);
-          ++ts.cnt;
-          if ((1u << rec_mbucket<MT>(r)) >= (uint32_t)p.k) ts.thr = dist;   // one group bounds the k-th distance
-        }
-      }
-    } else {
-      const uint32_t t0 = __ldg(p.t0_tup_off + leaf);
-      const uint32_t t1 = __ldg(p.t0_tup_off + leaf + 1);
-      for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
-        if (topk && ((g - t0) & 31) == 31) refresh_if_needed(e);
-        float dd = dist;
-        for (int tt = 1; tt < p.T; ++tt) {
-          const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
-          dd = dd + e.part[(size_t)p.part_base[tt] + (size_t)lf * 32 + lane];
-        }
-        const uint32_t mult = topk ? __ldg(p.group_mult + g) : 0u;
-        emit_group(e, dd, g, mult);
-      }
-    }
+  auto shfl_rec = [&](const uint4& mine, int j) {
+    uint4 r;
+    r.x = __shfl_sync(FULLMASK, mine.x, j);
+    r.y = (MT > 2) ? __shfl_sync(FULLMASK, mine.y, j) : 0u;
+    r.z = (MT > 4) ? __shfl_sync(FULLMASK, mine.z, j) : 0u;
+    r.w = __shfl_sync(FULLMASK, mine.w, j);   // levels 6-7, or the LCP when MT < 8
+    return r;
+  };
+  auto load_batch = [&](uint32_t base, uint32_t end) {
+    return (base + lane < end) ? __ldg(rec + base + lane) : make_uint4(0u, 0u, 0u, 0u);
   };
   auto batch_end = [&]() {
     if (topk && ROLE != 0) {   // prune full buffers; share the threshold with the CTA's other warps
@@ -863,41 +883,84 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
         const unsigned mine = __float_as_uint(e.ts.thr);
         atomicMin(&sm.thr[lane], mine);
         unsigned t = *((volatile unsigned*)&sm.thr[lane]);
-        if (p.qthr) t = min(t, atomicMin(p.qthr + e.q, t));
+        if (p.qthr_shared) t = min(t, atomicMin(p.qthr + e.q, t));
         e.ts.thr = __uint_as_float(t);
       }
     }
   };
-#if ET_SCAN_VARIANT == 3
-  uint4 nxt = (a + lane < b) ? __ldg(rec + a + lane) : make_uint4(0u, 0u, 0u, 0u);
-  for (uint32_t base = a; base < b; base += 32) {
-    const uint4 mine = nxt;
-    const uint32_t nb = base + 32 + lane;
-    nxt = (nb < b) ? __ldg(rec + nb) : make_uint4(0u, 0u, 0u, 0u);   // next batch in flight
-    const int n = (int)min(32u, b - base);
-    for (int j = 0; j < n; ++j) {
-      uint4 r;
-      r.x = __shfl_sync(FULLMASK, mine.x, j);
-      r.y = (MT > 2) ? __shfl_sync(FULLMASK, mine.y, j) : 0u;
-      r.z = (MT > 4) ? __shfl_sync(FULLMASK, mine.z, j) : 0u;
-      r.w = __shfl_sync(FULLMASK, mine.w, j);   // levels 6-7, or the LCP when MT < 8
-      leaf_body(base + j, r);
+  if constexpr (ROLE == 2) {
+    // E-Forest tree 0: one stream; each leaf walks its tuples (data-dependent loop)
+    float v[MT];
+#pragma unroll
+    for (int l = 0; l < MT; ++l) v[l] = 0.f;
+    uint4 nxt = load_batch(a, b);
+    for (uint32_t base = a; base < b; base += 32) {
+      const uint4 mine = nxt;
+      nxt = load_batch(base + 32, b);
+      const uint32_t tl = (base + lane < b) ? base + lane : b - 1;
+      const uint32_t my_t0 = __ldg(p.t0_tup_off + tl), my_t1 = __ldg(p.t0_tup_off + tl + 1);
+      const int n = (int)min(32u, b - base);
+      for (int j = 0; j < n; ++j) {
+        const uint4 r = shfl_rec(mine, j);
+        const uint32_t leaf = base + j;
+        const uint32_t pl = (leaf == a) ? 0u : rec_lcp<MT>(r);
+        const float dist = dc_leaf<MT>(v, r, pl, true, lane4, tq);
+        const uint32_t t0 = __shfl_sync(FULLMASK, my_t0, j), t1 = __shfl_sync(FULLMASK, my_t1, j);
+        for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
+          if (topk && ((g - t0) & 31) == 31) refresh_if_needed(e);
+          float dd = dist;
+          for (int tt = 1; tt < p.T; ++tt) {
+            const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
+            dd = dd + e.part[(size_t)p.part_base[tt] + (size_t)lf * 32 + lane];
+          }
+          const uint32_t mult = topk ? __ldg(p.group_mult + g) : 0u;
+          emit_group(e, dd, g, mult);
+        }
+      }
+      batch_end();
     }
-    batch_end();
+  } else {
+    const uint32_t m = a + (b - a + 1) / 2;   // halves [a, m) and [m, b); |[m, b)| <= |[a, m)|
+    float v0[MT], v1[MT];
+#pragma unroll
+    for (int l = 0; l < MT; ++l) { v0[l] = 0.f; v1[l] = 0.f; }
+    uint4 nx0 = load_batch(a, m), nx1 = load_batch(m, b);
+    auto emit = [&](uint32_t leaf, float dist, const uint4& r, bool valid) {
+      if constexpr (ROLE == 0) {
+        if (valid) e.part[(size_t)p.part_base[e.t] + (size_t)leaf * 32 + lane] = dist;
+      } else {
+        if (p.mode == kModeFull) {
+          if (valid) p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + leaf] = dist;   // query-major rows
+        } else {
+          TopkState& ts = e.ts;
+          const bool em = valid && ts.active && dist <= ts.thr;
+          if (em) ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), leaf);
+          ts.cnt += em ? 1 : 0;
+          // one group alone (2^bucket <= multiplicity ids) bounds the k-th distance
+          if (em && (1u << rec_mbucket<MT>(r)) >= (uint32_t)p.k) ts.thr = dist;
+        }
+      }
+    };
+    for (uint32_t off = 0; a + off < m; off += 32) {
+      const uint4 mine0 = nx0, mine1 = nx1;
+      nx0 = load_batch(a + off + 32, m);
+      nx1 = load_batch(m + off + 32, b);
+      const int n0 = (int)min(32u, m - (a + off));
+      const int n1 = (m + off < b) ? (int)min(32u, b - (m + off)) : 0;
+      for (int j = 0; j < n0; ++j) {
+        const uint4 r0 = shfl_rec(mine0, j), r1 = shfl_rec(mine1, j);
+        const uint32_t leaf0 = a + off + j, leaf1 = m + off + j;
+        const bool ok1 = j < n1;
+        const uint32_t pl0 = (off + j == 0) ? 0u : rec_lcp<MT>(r0);   // range starts: rebuild the path
+        const uint32_t pl1 = (off + j == 0) ? 0u : rec_lcp<MT>(r1);
+        const float d0 = dc_leaf<MT>(v0, r0, pl0, true, lane4, tq);
+        const float d1 = dc_leaf<MT>(v1, r1, pl1, ok1, lane4, tq);
+        emit(leaf0, d0, r0, true);
+        emit(leaf1, d1, r1, ok1);
+      }
+      batch_end();
+    }
   }
-#else
-  uint4 r0 = __ldg(rec + a);
-  uint4 r1 = (a + 1 < b) ? __ldg(rec + a + 1) : make_uint4(0u, 0u, 0u, 0u);
-  for (uint32_t leaf = a; leaf < b; ++leaf) {
-    if (((leaf - a) & 7u) == 0 && leaf + 16 < b)                     // keep L1 ahead of the loads
-      asm volatile("prefetch.global.L1 [%0];" :: "l"(rec + leaf + 16));
-    const uint4 r = r0;
-    r0 = r1;
-    r1 = (leaf + 2 < b) ? __ldg(rec + leaf + 2) : make_uint4(0u, 0u, 0u, 0u);
-    leaf_body(leaf, r);
-    if (((leaf - a) & 31u) == 31u || leaf + 1 == b) batch_end();
-  }
-#endif
 }
 
 template <int ROLE>
@@ -940,6 +1003,20 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   int MTmax = 0;
   for (int t = 0; t < p.T; ++t) MTmax = max(MTmax, p.tree[t].MT);
   const int smem_levels = (MTmax == 8) ? 7 : MTmax;
+  // resident build of the first tree: stage the queries asynchronously now
+  constexpr bool kResident = (SS == kDC && MTC > 0);
+  const bool staged = kResident && !p.luts && !p.chunk_cell;
+  if constexpr (kResident) {
+    if (staged) {
+      const int MTf = p.tree[p.T - 1].MT;
+      const size_t reg = ((size_t)smem_levels * 256 * 32 * 4 > (size_t)kFinRegion) ? (size_t)smem_levels * 256 * 32 * 4
+                                                                                    : (size_t)kFinRegion;
+      const uint32_t base = smem_u32(smem_raw);
+      const uint32_t region_s = base + ((uint32_t)(MTf - 1 - (MTf == 8 ? 1 : 0)) << 15);
+      const uint32_t stage_s = base + (uint32_t)reg + 32u * 4u + 32u * 4u;   // = sm.stage below
+      stage_async<SS, MTC>(p, p.T - 1, chunk, p.n_units / p.S, region_s, stage_s);
+    }
+  }
   SmemScan sm;
   sm.tab = reinterpret_cast<float*>(smem_raw);
   const size_t region = ((size_t)smem_levels * 256 * 32 * 4 > (size_t)kFinRegion) ? (size_t)smem_levels * 256 * 32 * 4
@@ -1002,7 +1079,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     bool level0_done = false;   // resident build copies level 0 to TMEM itself
     if constexpr (SS == kDC && MTC > 0) {
       if (p.luts) { build_tables<SS>(p, sm, t, unit, nq, cell); __syncthreads(); }
-      else { phase_mark(unit, 1); build_tables_resident<SS, MTC>(p, sm, t, unit, nq, cell); level0_done = true; phase_mark(unit, 2); }
+      else {
+        phase_mark(unit, 1);
+        build_tables_resident<SS, MTC>(p, sm, t, unit, nq, cell, staged && t == p.T - 1);
+        level0_done = true;
+        phase_mark(unit, 2);
+      }
     } else {
       build_tables<SS>(p, sm, t, unit, nq, cell);
       __syncthreads();
@@ -1041,6 +1123,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   phase_mark(unit, 3);
   if (use_tmem && warp == 0) tmem_dealloc(sm.tmem);
 
+  if (p.mode == kModeTopk && p.qthr && !p.qthr_shared && warp == 0 && sm.qidx[lane] >= 0)
+    p.qthr[sm.qidx[lane]] = sm.thr[lane];   // the query's only unit: its final threshold
   if (p.mode == kModeTopk && !p.compact) {
     // per-warp candidate lists stay where the scan wrote them: lane L's 16
     // buffers are contiguous, counts at cand_cnt[(unit*32 + L)*kWarps + warp]
