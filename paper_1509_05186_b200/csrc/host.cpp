@@ -943,7 +943,10 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   // register fast path when groups are large (few candidates per query)
   fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
   sp.compact = !fp.fast;
-  if (false && pl.S == 1) {   // fused finalize (kept for experiments; the separate kernel hides latency better)
+  // Finalize inside the scan kernel (pl.S == 1 && fp.fast) is exact too, but its
+  // latency-bound tail runs with the SM otherwise idle (measured +30 us on c2):
+  // the separate high-occupancy kernel wins, so the fused path stays off.
+  if (false && pl.S == 1 && fp.fast) {
     sp.fuse_fin = 1;
     sp.fin = fp;
     cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");

@@ -274,14 +274,14 @@ __device__ __forceinline__ float* tab_slot(const SmemScan& sm, float* lut0, int 
 
 // Inner loop of one build pass: codeword chunk c[0..NJ) (registers) against
 // query slots i = g, g+G, ... read from the staged chunk (broadcast loads).
-template <int NJ>
+template <int NJ, int DC = kDC>
 __device__ __forceinline__ void build_pass_fixed(const SmemScan& sm, float* lut0, int l, int lv0, int k,
                                                  bool kvalid, const float* c, int nq, int g, int G,
                                                  bool first) {
   int i = g;
   for (; i + G < nq; i += 2 * G) {   // two independent FMA chains
-    const float* x0 = sm.stage + i * kDC;
-    const float* x1 = sm.stage + (i + G) * kDC;
+    const float* x0 = sm.stage + i * DC;
+    const float* x1 = sm.stage + (i + G) * DC;
     float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
     float* o1 = tab_slot(sm, lut0, l, lv0, k, i + G);
     float a0 = 0.f, a1 = 0.f;
@@ -296,7 +296,7 @@ __device__ __forceinline__ void build_pass_fixed(const SmemScan& sm, float* lut0
     if (kvalid) { *o0 = a0; *o1 = a1; }
   }
   if (i < nq) {
-    const float* x0 = sm.stage + i * kDC;
+    const float* x0 = sm.stage + i * DC;
     float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
     float a0 = (!first && kvalid) ? *o0 : 0.f;
 #pragma unroll
@@ -544,7 +544,7 @@ __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const
 // codeword chunk in registers) against a share of the queries.  Entries are
 // accumulated across chunks in place, so every entry is the j-ascending fp32
 // FMA chain sum_j (x_j - c_j)^2 regardless of the chunking.
-template <int SS>
+template <int SS, int DC = kDC>
 __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq, int cell) {
   const TreeDev& tr = p.tree[t];
   const int MT = tr.MT;
@@ -566,17 +566,17 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
     }
     return;
   }
-  const int npl = (s + kDC - 1) / kDC;          // passes per level
+  const int npl = (s + DC - 1) / DC;            // passes per level
   const int P = MT * npl;
   const int G = max(1, kWarps / nb);            // query groups
   const int kb = warp % nb, g = warp / nb;
   const bool computes = g < G;
   // staging element of this thread: query slot si, dimension sj of the chunk
-  const int si = threadIdx.x / kDC, sj = threadIdx.x % kDC;
+  const int si = threadIdx.x / DC, sj = threadIdx.x % DC;
   const int sq = (si < nq) ? sm.qidx[si] : -1;
   auto fetch = [&](int pass) -> float {
     const int l = pass / npl, jc = pass - l * npl;
-    const int j = jc * kDC + sj;
+    const int j = jc * DC + sj;
     if (sq < 0 || j >= s) return 0.f;
     const int m = p.layer_sub[tr.layer0 + l];
     float v = __ldg(p.queries + (size_t)sq * d + (size_t)m * s + j);
@@ -586,34 +586,45 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
   // codeword chunk of pass `pass` for this lane's codeword (registers)
   const int k = kb * 32 + lane;
   const bool kvalid = computes && k < K;
-  auto fetch_cw = [&](int pass, float (&c)[kDC]) {
+  auto fetch_cw = [&](int pass, float (&c)[DC]) {
     const int l = pass / npl, jc = pass - l * npl;
-    const int j0 = jc * kDC;
-    const int nj = min(kDC, s - j0);
+    const int j0 = jc * DC;
+    const int nj = min(DC, s - j0);
     const int m = p.layer_sub[tr.layer0 + l];
     const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s + j0;
+    if (p.vec4 && (s & 3) == 0) {   // 16-byte aligned rows: float4 loads
 #pragma unroll
-    for (int j = 0; j < kDC; ++j) c[j] = (kvalid && j < nj) ? __ldg(crow + j) : 0.f;
+      for (int j = 0; j < DC; j += 4) {
+        const float4 v = (j < nj) ? __ldg(reinterpret_cast<const float4*>(crow + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < DC; ++j) c[j] = (j < nj) ? __ldg(crow + j) : 0.f;
+    }
   };
-  float cw[kDC], cwn[kDC];
+  // DC == kDC: the next pass's codeword chunk is prefetched into registers;
+  // wide passes (DC > kDC, few queries) load it at the pass start instead
+  constexpr bool kPrefetchCw = (DC == kDC);
+  float cw[DC], cwn[kPrefetchCw ? DC : 1];
   fetch_cw(0, cw);
   float nxt = fetch(0);
   __syncthreads();                              // previous users of the stage are done
   if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
   __syncthreads();
   for (int pass = 0; pass < P; ++pass) {
-    if (pass + 1 < P) {                         // prefetch the next pass: stage values + codeword chunk
+    if (pass + 1 < P) {                         // prefetch the next pass: stage values (+ codeword chunk)
       nxt = fetch(pass + 1);
-      fetch_cw(pass + 1, cwn);
+      if constexpr (kPrefetchCw) fetch_cw(pass + 1, cwn);
     }
     const int l = pass / npl, jc = pass - l * npl;
-    const int nj = min(kDC, s - jc * kDC);
+    const int nj = min(DC, s - jc * DC);
     if (computes) {
-      if constexpr (SS > 0 && SS % kDC == 0) {
-        build_pass_fixed<kDC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
+      if constexpr (SS > 0 && SS % DC == 0) {
+        build_pass_fixed<DC, DC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
       } else if constexpr (SS > 0) {
-        if (nj == kDC) build_pass_fixed<kDC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
-        else build_pass_fixed<(SS % kDC) ? (SS % kDC) : kDC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
+        if (nj == DC) build_pass_fixed<DC, DC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
+        else build_pass_fixed<(SS % DC) ? (SS % DC) : DC, DC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
       } else {
         build_pass_generic(sm, lut0, l, lv0, k, kvalid, cw, nj, nq, g, G, jc == 0);
       }
@@ -621,8 +632,12 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
     __syncthreads();
     if (pass + 1 < P) {
       if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
+      if constexpr (kPrefetchCw) {
 #pragma unroll
-      for (int j = 0; j < kDC; ++j) cw[j] = cwn[j];
+        for (int j = 0; j < DC; ++j) cw[j] = cwn[j];
+      } else {
+        fetch_cw(pass + 1, cw);
+      }
     }
     __syncthreads();
   }
@@ -989,6 +1004,7 @@ __device__ __forceinline__ void scan_any(EmitCtx& e, const SmemScan& sm, const T
 
 struct FinWarp;
 __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q);
+__device__ void finalize_fused(const FinParams& p, unsigned char* smem, const int* qidx, int nq);
 
 template <int SS, int MTC, bool FOREST>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant__ ScanParams p) {
@@ -1171,11 +1187,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       if (lane < kWarps) p.cand_cnt[((size_t)unit * 32 + L) * kWarps + lane] = (lane == 0) ? n : 0;
       if (lane == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + L] = __uint_as_float(tb);
     }
-    if (p.fuse_fin) {
-      __syncthreads();
-      FinWarp* fw = reinterpret_cast<FinWarp*>(smem_raw + (size_t)warp * kFinWarpBytes);
-      for (int i = warp; i < nq; i += kWarps) finalize_query(p.fin, *fw, sm.qidx[i]);
-    }
+  }
+  if (p.mode == kModeTopk && p.fuse_fin) {   // every query of this chunk was scanned by this CTA alone
+    __threadfence_block();
+    __syncthreads();
+    finalize_fused(p.fin, smem_raw, sm.qidx, nq);
   }
   phase_mark(unit, 4);
 }
@@ -1313,7 +1329,7 @@ struct CandSrc {
     const int nl = (s1 - s0) * p->S * kWarps;
     for (int li = 0; li < nl; ++li) {
       const size_t ul = fin_list(*p, q, s0, li);
-      const int c = __ldg(p->cand_cnt + ul);
+      const int c = __ldcg(p->cand_cnt + ul);
       const uint2* eb = p->cand + ul * p->B;
       for (int i = lane; i < c; i += 32) {
         const uint2 v = eb[i];
@@ -1333,13 +1349,13 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
   // 1. threshold prefilter: min over the query's units of their final thresholds
   float thr = __int_as_float(0x7f800000);
   if (p.qthr) {   // every unit of the query folded its final threshold into qthr
-    thr = __uint_as_float(__ldg(p.qthr + q));
+    thr = __uint_as_float(__ldcg(p.qthr + q));
   } else if (unit_thr) {
     for (int j = s0; j < s1; ++j) {
       const int slot = fin_slot(p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
       for (int sg = lane; sg < p.S; sg += 32)
-        thr = fminf(thr, __ldg(unit_thr + (size_t)(chunk * p.S + sg) * 32 + ln));
+        thr = fminf(thr, __ldcg(unit_thr + (size_t)(chunk * p.S + sg) * 32 + ln));
     }
     for (int o = 16; o > 0; o >>= 1) thr = fminf(thr, __shfl_xor_sync(FULLMASK, thr, o));
   }
@@ -1360,7 +1376,7 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
       int myc = 0;
       if (li < nl) {
         ul = fin_list(p, q, s0, li);
-        myc = __ldg(p.cand_cnt + ul);
+        myc = __ldcg(p.cand_cnt + ul);
       }
       int inc = myc;
 #pragma unroll
@@ -1694,26 +1710,23 @@ __device__ __forceinline__ void bitonic32(unsigned long long& a) {
   }
 }
 
-__global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __grid_constant__ FinParams p) {
-  extern __shared__ __align__(16) unsigned char fsm_raw[];
-  if (threadIdx.x == 0) *reinterpret_cast<int*>(fsm_raw) = 0;
-  __syncthreads();
+// One query, one warp.  own_fw: this warp's private slow-path scratch (the
+// scan kernel's fused finalize) or null (the standalone kernel's locked one).
+__device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t q, FinWarp* own_fw) {
   const int lane = lane_id();
-  const int64_t q = (int64_t)blockIdx.x * kFastWarps + warp_id();
-  if (q >= p.Q) return;
   const int k = p.k;
   const int s0 = fin_s0(p, q), s1 = fin_s1(p, q);
 
   // 1. threshold prefilter (as the slow path)
   float thr = __int_as_float(0x7f800000);
   if (p.qthr) {
-    thr = __uint_as_float(__ldg(p.qthr + q));
+    thr = __uint_as_float(__ldcg(p.qthr + q));
   } else if (p.unit_thr) {
     for (int j = s0; j < s1; ++j) {
       const int slot = fin_slot(p, q, j);
       const int chunk = slot >> 5, ln = slot & 31;
       for (int sg = lane; sg < p.S; sg += 32)
-        thr = fminf(thr, __ldg(p.unit_thr + (size_t)(chunk * p.S + sg) * 32 + ln));
+        thr = fminf(thr, __ldcg(p.unit_thr + (size_t)(chunk * p.S + sg) * 32 + ln));
     }
     for (int o = 16; o > 0; o >>= 1) thr = fminf(thr, __shfl_xor_sync(FULLMASK, thr, o));
   }
@@ -1730,7 +1743,7 @@ __global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __
     int myc = 0;
     if (li < nl) {
       ul = fin_list(p, q, s0, li);
-      myc = __ldg(p.cand_cnt + ul);
+      myc = __ldcg(p.cand_cnt + ul);
     }
     int inc = myc;
 #pragma unroll
@@ -1767,7 +1780,10 @@ __global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __
       n += c;
     }
   }
-  if (overflow) { finalize_locked(p, q); return; }
+  if (overflow) {
+    if (own_fw) finalize_query(p, *own_fw, q); else finalize_locked(p, q);
+    return;
+  }
 
   // 3. offsets / multiplicities of the held groups (one dependent load)
   uint32_t o0a = 0, mua = 0, o0b = 0, mub = 0;
@@ -1812,7 +1828,10 @@ __global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __
   const uint32_t nA = (lane == 31) ? dB_first : dA_next;
   const bool tieA = (lane <= last) && (lane + 1 < n) && nA == dA;
   const bool tieB = (32 + lane <= last) && (32 + lane + 1 < n) && lane < 31 && dB_next == dB;
-  if (__any_sync(FULLMASK, tieA || tieB)) { finalize_locked(p, q); return; }
+  if (__any_sync(FULLMASK, tieA || tieB)) {
+    if (own_fw) finalize_query(p, *own_fw, q); else finalize_locked(p, q);
+    return;
+  }
 
   // 5. output: the selected groups in distance order, ids ascending within each
   float* od = p.out_dist + (size_t)q * k;
@@ -1836,6 +1855,24 @@ __global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __
   for (uint32_t i = written + lane; i < (uint32_t)k; i += 32) {
     od[i] = __int_as_float(0x7f800000);
     oi[i] = -1;
+  }
+}
+
+__global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __grid_constant__ FinParams p) {
+  extern __shared__ __align__(16) unsigned char fsm_raw[];
+  if (threadIdx.x == 0) *reinterpret_cast<int*>(fsm_raw) = 0;
+  __syncthreads();
+  const int64_t q = (int64_t)blockIdx.x * kFastWarps + warp_id();
+  if (q >= p.Q) return;
+  finalize_fast_query(p, q, nullptr);
+}
+
+// Fused finalize (scan kernel, every query of the CTA scanned by it alone).
+__device__ void finalize_fused(const FinParams& p, unsigned char* smem, const int* qidx, int nq) {
+  FinWarp* fw = reinterpret_cast<FinWarp*>(smem + (size_t)warp_id() * sizeof(FinWarp));
+  for (int i = warp_id(); i < nq; i += kWarps) {
+    if (p.fast) finalize_fast_query(p, qidx[i], fw);
+    else finalize_query(p, *fw, qidx[i]);
   }
 }
 
