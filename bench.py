@@ -116,14 +116,35 @@ def workload_config(name):
     return cfg
 
 
+def _gen_chunk(args):
+    """Worker: base vectors [s, s + n) of config ``name`` (block-addressed, so
+    any worker can produce any range)."""
+    name, s, n = args
+    cfg = synth.CONFIGS[name]
+    return s, synth.base(cfg, s, n, means=_gen_chunk.means)
+
+
+def _gen_init(name):
+    _gen_chunk.means = synth.mixture_means(synth.CONFIGS[name])
+
+
 def gen_base_encode(cfg, cb_dev, means, dev, chunk=1 << 18):
-    """Generate the base on the host block by block, encode each block on the
-    GPU with et_encode; returns host uint8 codes [N, M]."""
+    """Generate the base on the host block by block (a process pool for large
+    N: 10^8 x 128 is ~11 min on one core), encode each block on the GPU with
+    et_encode; returns host uint8 codes [N, M]."""
     import torch
     from paper_1509_05186_b200 import api
     codes = np.empty((cfg.N, cfg.M), dtype=np.uint8)
-    for s in range(0, cfg.N, chunk):
-        n = min(chunk, cfg.N - s)
+    jobs = [(cfg.name, s, min(chunk, cfg.N - s)) for s in range(0, cfg.N, chunk)]
+    workers = min(len(jobs), max(1, (os.cpu_count() or 1) - 1), 48)
+    if cfg.N >= (1 << 23) and workers > 1 and synth.CONFIGS.get(cfg.name) == cfg:
+        import multiprocessing as mp
+        with mp.get_context("spawn").Pool(workers, initializer=_gen_init, initargs=(cfg.name,)) as pool:
+            for s, x in pool.imap(_gen_chunk, jobs, chunksize=1):
+                xd = torch.from_numpy(x).to(dev)
+                codes[s:s + len(x)] = api.et_encode(cb_dev, xd).cpu().numpy()
+        return codes
+    for _, s, n in jobs:
         x = torch.from_numpy(synth.base(cfg, s, n, means=means)).to(dev)
         codes[s:s + n] = api.et_encode(cb_dev, x).cpu().numpy()
     return codes

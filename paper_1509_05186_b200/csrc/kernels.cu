@@ -921,15 +921,41 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
         const uint32_t pl = (leaf == a) ? 0u : rec_lcp<MT>(r);
         const float dist = dc_leaf<MT>(v, r, pl, true, lane4, tq);
         const uint32_t t0 = __shfl_sync(FULLMASK, my_t0, j), t1 = __shfl_sync(FULLMASK, my_t1, j);
-        for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
-          if (topk && ((g - t0) & 31) == 31) refresh_if_needed(e);
-          float dd = dist;
-          for (int tt = 1; tt < p.T; ++tt) {
-            const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
-            dd = dd + e.part[(size_t)p.part_base[tt] + (size_t)lf * 32 + lane];
+        if (p.T == 2) {
+          // E-Forest join (A13): 32 tuples at a time -- their tree-1 leaves and
+          // multiplicities in one coalesced load each, then the per-query
+          // partials 8 tuples at a time (independent loads in flight)
+          const float* part1 = e.part + (size_t)p.part_base[1] + lane;
+          for (uint32_t g0 = t0; g0 < t1; g0 += 32) {
+            const int n = (int)min(32u, t1 - g0);
+            const uint32_t my_lf = (lane < n) ? __ldg(p.tup_leaf[1] + g0 + lane) : 0u;
+            const uint32_t my_mu = (topk && lane < n) ? __ldg(p.group_mult + g0 + lane) : 0u;
+            for (int u0 = 0; u0 < n; u0 += 8) {
+              float pv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const uint32_t lf = __shfl_sync(FULLMASK, my_lf, u0 + u);
+                pv[u] = (u0 + u < n) ? part1[(size_t)lf * 32] : 0.f;
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const uint32_t mult = __shfl_sync(FULLMASK, my_mu, u0 + u);
+                if (u0 + u < n) emit_group(e, dist + pv[u], g0 + u0 + u, mult);   // tree order p0 + p1
+              }
+            }
+            if (topk) refresh_if_needed(e);
           }
-          const uint32_t mult = topk ? __ldg(p.group_mult + g) : 0u;
-          emit_group(e, dd, g, mult);
+        } else {
+          for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
+            if (topk && ((g - t0) & 31) == 31) refresh_if_needed(e);
+            float dd = dist;
+            for (int tt = 1; tt < p.T; ++tt) {
+              const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
+              dd = dd + e.part[(size_t)p.part_base[tt] + (size_t)lf * 32 + lane];
+            }
+            const uint32_t mult = topk ? __ldg(p.group_mult + g) : 0u;
+            emit_group(e, dd, g, mult);
+          }
         }
       }
       batch_end();
