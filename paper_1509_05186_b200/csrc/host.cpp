@@ -391,6 +391,10 @@ static et_index* build_forest(const uint8_t* codes_in, const int32_t* ids, int64
     finish_tree(ix.get(), 0, h);
     if (T > 1) {
       ix->t0_tup_off.upload(tup_off);
+      std::vector<uint32_t> tl0(G);   // tree-0 leaf of each tuple
+      for (size_t i = 0; i + 1 < tup_off.size(); ++i)
+        for (uint32_t g2 = tup_off[i]; g2 < tup_off[i + 1]; ++g2) tl0[g2] = (uint32_t)i;
+      ix->tup_leaf[0].upload(tl0);
       look += (double)G;   // one join per tuple
     }
   }
@@ -589,7 +593,8 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   pl.n_units = pl.n_chunks * pl.S;
   pl.B = topk_B(std::max(1, k));
   int64_t off = 0;
-  for (int t = 1; t < ix->T; ++t) { pl.part_base[t] = off; off += ix->n_leaves[t] * 32; }
+  if (ix->T > 1)   // forests: per-leaf partials of every tree (the join reads them)
+    for (int t = 0; t < ix->T; ++t) { pl.part_base[t] = off; off += ix->n_leaves[t] * 32; }
   pl.part_stride = off;
   return pl;
 }

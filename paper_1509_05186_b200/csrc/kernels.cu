@@ -736,7 +736,7 @@ struct TopkState {
 
 struct EmitCtx {
   const ScanParams* p;
-  int role;           // 0: forest partial (tree t>=1), 1: tree-0 leaves are the groups, 2: forest tuples
+  int role;           // 0: forest per-leaf partials (every tree), 1: single tree, leaves are the groups
   int t;              // tree index for role 0
   int unit, chunk;
   int q;              // query of this lane (-1: idle lane)
@@ -903,64 +903,7 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
       }
     }
   };
-  if constexpr (ROLE == 2) {
-    // E-Forest tree 0: one stream; each leaf walks its tuples (data-dependent loop)
-    float v[MT];
-#pragma unroll
-    for (int l = 0; l < MT; ++l) v[l] = 0.f;
-    uint4 nxt = load_batch(a, b);
-    for (uint32_t base = a; base < b; base += 32) {
-      const uint4 mine = nxt;
-      nxt = load_batch(base + 32, b);
-      const uint32_t tl = (base + lane < b) ? base + lane : b - 1;
-      const uint32_t my_t0 = __ldg(p.t0_tup_off + tl), my_t1 = __ldg(p.t0_tup_off + tl + 1);
-      const int n = (int)min(32u, b - base);
-      for (int j = 0; j < n; ++j) {
-        const uint4 r = shfl_rec(mine, j);
-        const uint32_t leaf = base + j;
-        const uint32_t pl = (leaf == a) ? 0u : rec_lcp<MT>(r);
-        const float dist = dc_leaf<MT>(v, r, pl, true, lane4, tq);
-        const uint32_t t0 = __shfl_sync(FULLMASK, my_t0, j), t1 = __shfl_sync(FULLMASK, my_t1, j);
-        if (p.T == 2) {
-          // E-Forest join (A13): 32 tuples at a time -- their tree-1 leaves and
-          // multiplicities in one coalesced load each, then the per-query
-          // partials 8 tuples at a time (independent loads in flight)
-          const float* part1 = e.part + (size_t)p.part_base[1] + lane;
-          for (uint32_t g0 = t0; g0 < t1; g0 += 32) {
-            const int n = (int)min(32u, t1 - g0);
-            const uint32_t my_lf = (lane < n) ? __ldg(p.tup_leaf[1] + g0 + lane) : 0u;
-            const uint32_t my_mu = (topk && lane < n) ? __ldg(p.group_mult + g0 + lane) : 0u;
-            for (int u0 = 0; u0 < n; u0 += 8) {
-              float pv[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const uint32_t lf = __shfl_sync(FULLMASK, my_lf, u0 + u);
-                pv[u] = (u0 + u < n) ? part1[(size_t)lf * 32] : 0.f;
-              }
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const uint32_t mult = __shfl_sync(FULLMASK, my_mu, u0 + u);
-                if (u0 + u < n) emit_group(e, dist + pv[u], g0 + u0 + u, mult);   // tree order p0 + p1
-              }
-            }
-            if (topk) refresh_if_needed(e);
-          }
-        } else {
-          for (uint32_t g = t0; g < t1; ++g) {   // E-Forest join, tree order (A13)
-            if (topk && ((g - t0) & 31) == 31) refresh_if_needed(e);
-            float dd = dist;
-            for (int tt = 1; tt < p.T; ++tt) {
-              const uint32_t lf = __ldg(p.tup_leaf[tt] + g);
-              dd = dd + e.part[(size_t)p.part_base[tt] + (size_t)lf * 32 + lane];
-            }
-            const uint32_t mult = topk ? __ldg(p.group_mult + g) : 0u;
-            emit_group(e, dd, g, mult);
-          }
-        }
-      }
-      batch_end();
-    }
-  } else {
+  {
     const uint32_t m = a + (b - a + 1) / 2;   // halves [a, m) and [m, b); |[m, b)| <= |[a, m)|
     float v0[MT], v1[MT];
 #pragma unroll
@@ -1001,6 +944,67 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
       }
       batch_end();
     }
+  }
+}
+
+// Prune full candidate buffers and share the lanes' thresholds with the CTA's
+// other warps (shared memory) and, when a query spans several units, with
+// every unit scanning it (global per-query atomicMin).
+__device__ __forceinline__ void share_threshold(EmitCtx& e, const SmemScan& sm) {
+  const ScanParams& p = *e.p;
+  const int lane = lane_id();
+  refresh_if_needed(e);
+  if (e.ts.active) {
+    atomicMin(&sm.thr[lane], __float_as_uint(e.ts.thr));
+    unsigned t = *((volatile unsigned*)&sm.thr[lane]);
+    if (p.qthr_shared) t = min(t, atomicMin(p.qthr + e.q, t));
+    e.ts.thr = __uint_as_float(t);
+  }
+}
+
+// E-Forest join (reading A13): every tuple -- one distinct full
+// code, i.e. one group -- gets dist = ((p_0 + p_1) + ...) summed in tree order
+// from the per-tree partials of its leaves (written by the trees' scans).
+// Tuples [ga, gb) of this warp, 32 at a time: their leaves and multiplicities
+// in one coalesced load each, then the per-query partials (coalesced across
+// lanes) eight tuples at a time.
+__device__ void join_tuples(EmitCtx& e, const SmemScan& sm, uint32_t ga, uint32_t gb) {
+  const ScanParams& p = *e.p;
+  const int lane = lane_id();
+  const bool topk = p.mode == kModeTopk;
+  for (uint32_t g0 = ga; g0 < gb; g0 += 32) {
+    const int n = (int)min(32u, gb - g0);
+    uint32_t my_l[kMaxTrees];
+#pragma unroll
+    for (int t = 0; t < kMaxTrees; ++t) my_l[t] = (t < p.T && lane < n) ? __ldg(p.tup_leaf[t] + g0 + lane) : 0u;
+    const uint32_t my_mu = (topk && lane < n) ? __ldg(p.group_mult + g0 + lane) : 0u;
+    for (int u0 = 0; u0 < n; u0 += 8) {
+      float acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t l0 = __shfl_sync(FULLMASK, my_l[0], u0 + u);
+        acc[u] = (u0 + u < n) ? e.part[(size_t)p.part_base[0] + (size_t)l0 * 32 + lane] : 0.f;
+      }
+#pragma unroll
+      for (int t = 1; t < kMaxTrees; ++t) {
+        if (t < p.T) {
+          float pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint32_t lt = __shfl_sync(FULLMASK, my_l[t], u0 + u);
+            pv[u] = (u0 + u < n) ? e.part[(size_t)p.part_base[t] + (size_t)lt * 32 + lane] : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = acc[u] + pv[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t mult = __shfl_sync(FULLMASK, my_mu, u0 + u);
+        if (u0 + u < n) emit_group(e, acc[u], g0 + u0 + u, mult);
+      }
+    }
+    if (topk) share_threshold(e, sm);
   }
 }
 
@@ -1152,8 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     e.t = t;
     if (wa < wb) {
       if constexpr (FOREST) {
-        if (t > 0) scan_any<MTC, 0>(e, sm, tr, wa, wb, lut0g);
-        else scan_any<MTC, 2>(e, sm, tr, wa, wb, lut0g);
+        scan_any<MTC, 0>(e, sm, tr, wa, wb, lut0g);   // per-leaf partials of every tree
       } else {
         scan_any<MTC, 1>(e, sm, tr, wa, wb, lut0g);
       }
@@ -1161,6 +1164,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     tmem_fence_before();
     __syncthreads();   // partials visible / tables free for the next tree
     tmem_fence_after();
+  }
+  if constexpr (FOREST) {   // the CTA's warps split the tuples evenly
+    const uint64_t G = (uint64_t)p.n_groups;
+    join_tuples(e, sm, (uint32_t)((G * warp) / kWarps), (uint32_t)((G * (warp + 1)) / kWarps));
   }
   phase_mark(unit, 3);
   if (use_tmem && warp == 0) tmem_dealloc(sm.tmem);
