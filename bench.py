@@ -56,7 +56,7 @@ def load_peaks():
 class ClockSampler:
     """Samples SM clock + throttle reasons via NVML in a background thread."""
 
-    def __init__(self, index=0, period=0.002):
+    def __init__(self, index=0, period=0.0005):
         self.samples = []
         self.reasons = set()
         self.max_mhz = None
