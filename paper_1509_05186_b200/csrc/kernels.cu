@@ -1786,31 +1786,40 @@ __device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t 
     }
     const int total = __shfl_sync(FULLMASK, inc, 31);
     const int excl = inc - myc;
-    for (int i0 = 0; i0 < total; i0 += 32) {
-      const int idx = i0 + lane;
-      int w = 0;
+    constexpr int kRounds = 4;   // candidate loads of four rounds in flight at once
+    for (int i00 = 0; i00 < total && !overflow; i00 += 32 * kRounds) {
+      uint2 vv[kRounds];
 #pragma unroll
-      for (int st = 16; st >= 1; st >>= 1) {
-        const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
-        if (w + st < 32 && o <= idx) w += st;
+      for (int rr = 0; rr < kRounds; ++rr) {
+        const int idx = i00 + rr * 32 + lane;
+        int w = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1) {
+          const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
+          if (w + st < 32 && o <= idx) w += st;
+        }
+        const int wo = __shfl_sync(FULLMASK, excl, w);
+        const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
+        vv[rr] = (idx < total) ? p.cand[ulw * p.B + (idx - wo)] : make_uint2(0xffffffffu, 0);
       }
-      const int wo = __shfl_sync(FULLMASK, excl, w);
-      const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
-      uint2 v = make_uint2(0xffffffffu, 0);
-      if (idx < total) v = p.cand[ulw * p.B + (idx - wo)];
-      const bool keep = (idx < total) && v.x <= tb;
-      const unsigned m = __ballot_sync(FULLMASK, keep);
-      const int c = __popc(m);
-      if (n + c > kFastCap) { overflow = true; break; }
-      // lane L receives the r-th kept entry, r = (L - n) mod 32, at position n + r
-      const int r = (lane - n) & 31;
-      const int src = (r < c) ? (int)__fns(m, 0, r + 1) : 0;
-      const uint32_t vx = __shfl_sync(FULLMASK, v.x, src);
-      const uint32_t vy = __shfl_sync(FULLMASK, v.y, src);
-      if (r < c) {
-        if (((n + r) >> 5) == 0) r0 = make_uint2(vx, vy); else r1 = make_uint2(vx, vy);
+#pragma unroll
+      for (int rr = 0; rr < kRounds; ++rr) {
+        const int idx = i00 + rr * 32 + lane;
+        const uint2 v = vv[rr];
+        const bool keep = (idx < total) && v.x <= tb;
+        const unsigned m = __ballot_sync(FULLMASK, keep);
+        const int c = __popc(m);
+        if (n + c > kFastCap) { overflow = true; break; }
+        // lane L receives the r-th kept entry, r = (L - n) mod 32, at position n + r
+        const int r = (lane - n) & 31;
+        const int src = (r < c) ? (int)__fns(m, 0, r + 1) : 0;
+        const uint32_t vx = __shfl_sync(FULLMASK, v.x, src);
+        const uint32_t vy = __shfl_sync(FULLMASK, v.y, src);
+        if (r < c) {
+          if (((n + r) >> 5) == 0) r0 = make_uint2(vx, vy); else r1 = make_uint2(vx, vy);
+        }
+        n += c;
       }
-      n += c;
     }
   }
   if (overflow) {
