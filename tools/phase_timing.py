@@ -13,7 +13,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-LIB = os.path.join(ROOT, "paper_1509_05186_b200", "_build", "phase", "libetree.so")
+LIB = os.environ.get("ET_PHASE_LIB") or os.path.join(ROOT, "paper_1509_05186_b200", "_build", "phase", "libetree.so")
 os.environ["ET_LIB_PATH"] = LIB
 
 import bench  # noqa: E402
