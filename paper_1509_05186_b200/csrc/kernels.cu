@@ -1358,15 +1358,40 @@ struct CandSrc {
       for (int i = lane; i < n; i += 32) f(key[i], grp[i], mul[i]);
       return;
     }
+    // 32 lists per round: counts loaded in parallel (lane = list), then the
+    // round's entries spread over the lanes (binary search on the prefix)
     const uint32_t tb = __float_as_uint(thr);
     const int nl = (s1 - s0) * p->S * kWarps;
-    for (int li = 0; li < nl; ++li) {
-      const size_t ul = fin_list(*p, q, s0, li);
-      const int c = __ldcg(p->cand_cnt + ul);
-      const uint2* eb = p->cand + ul * p->B;
-      for (int i = lane; i < c; i += 32) {
-        const uint2 v = eb[i];
-        if (v.x <= tb) f(v.x, v.y, __ldg(p->group_mult + v.y));
+    for (int l0 = 0; l0 < nl; l0 += 32) {
+      const int li = l0 + lane;
+      size_t ul = 0;
+      int myc = 0;
+      if (li < nl) {
+        ul = fin_list(*p, q, s0, li);
+        myc = __ldcg(p->cand_cnt + ul);
+      }
+      int inc = myc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULLMASK, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int total = __shfl_sync(FULLMASK, inc, 31);
+      const int excl = inc - myc;
+      for (int i0 = 0; i0 < total; i0 += 32) {
+        const int idx = i0 + lane;
+        int w = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1) {
+          const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
+          if (w + st < 32 && o <= idx) w += st;
+        }
+        const int wo = __shfl_sync(FULLMASK, excl, w);
+        const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
+        if (idx < total) {
+          const uint2 v = p->cand[ulw * p->B + (idx - wo)];
+          if (v.x <= tb) f(v.x, v.y, __ldg(p->group_mult + v.y));
+        }
       }
     }
   }

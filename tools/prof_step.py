@@ -28,7 +28,10 @@ def main():
     st = bench.prepare_ours(cfg, dev, 0, 1)
     ix = st["ix"]
     for _ in range(a.steps):
-        d, i = ix.et_etree_topk(cfg.topk, queries=st["q_dev"], codebooks=st["cb_dev"])
+        if cfg.ivf_nlist:
+            d, i = ix.et_ivf_topk(st["q_dev"], nprobe=cfg.ivf_nprobe, k=cfg.topk)
+        else:
+            d, i = ix.et_etree_topk(cfg.topk, queries=st["q_dev"], codebooks=st["cb_dev"])
     torch.cuda.synchronize()
     print("ok", d[0, :4].tolist(), i[0, :4].tolist())
 
