@@ -30,6 +30,9 @@ def main():
     for _ in range(a.steps):
         if cfg.ivf_nlist:
             d, i = ix.et_ivf_topk(st["q_dev"], nprobe=cfg.ivf_nprobe, k=cfg.topk)
+        elif cfg.topk == 0:   # full Q x N output (c1)
+            d = ix.et_etree_distances(queries=st["q_dev"], codebooks=st["cb_dev"])
+            i = d[:, :4].int()
         else:
             d, i = ix.et_etree_topk(cfg.topk, queries=st["q_dev"], codebooks=st["cb_dev"])
     torch.cuda.synchronize()
