@@ -1925,7 +1925,7 @@ __device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t 
   }
 }
 
-__global__ void __launch_bounds__(kFastWarps * 32) finalize_fast_kernel(const __grid_constant__ FinParams p) {
+__global__ void __launch_bounds__(kFastWarps * 32, 6) finalize_fast_kernel(const __grid_constant__ FinParams p) {
   extern __shared__ __align__(16) unsigned char fsm_raw[];
   if (threadIdx.x == 0) *reinterpret_cast<int*>(fsm_raw) = 0;
   __syncthreads();
