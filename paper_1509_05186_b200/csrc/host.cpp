@@ -683,6 +683,7 @@ static size_t ivf_ws_bytes(const et_index* ix, const Plan& pl, int64_t Q, int w)
 static void fill_scan_common(ScanParams& sp, const et_index* ix, const Plan& pl) {
   sp.M = ix->M; sp.K = ix->K;
   sp.layer_sub = ix->layer_sub_d.as<int>();
+  for (int l = 0; l < ix->M && l < kMaxTrees * kMaxMT; ++l) sp.lsub[l] = ix->layer_sub[l];
   sp.T = ix->T;
   for (int t = 0; t < ix->T; ++t) {
     sp.tree[t].MT = ix->stats[t].M;

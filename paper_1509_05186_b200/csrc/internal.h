@@ -62,7 +62,8 @@ struct ScanParams {
   const float* queries = nullptr;     // [Q][d]           (fused tables)
   const float* luts = nullptr;        // [Q][M][K]        (materialised tables) or null
   const float* coarse = nullptr;      // [nlist][d]       (IVF residual tables) or null
-  const int* layer_sub = nullptr;     // [M] subspace of each code byte (chunk order)
+  const int* layer_sub = nullptr;     // [M] subspace of each code byte (chunk order), device copy
+  int lsub[kMaxTrees * kMaxMT] = {};  // the same, by value (kernel parameters: no dependent load)
   int d = 0, M = 0, K = 0, s = 0;
   // ---- work decomposition ----
   int n_units = 0;                    // CTAs = n_chunks * S

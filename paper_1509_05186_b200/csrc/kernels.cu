@@ -390,7 +390,7 @@ __device__ __forceinline__ void stage_async(const ScanParams& p, int t, int chun
 #pragma unroll
   for (int l = 0; l < MT; ++l) {
     const uint32_t dst = (l < MT - 1) ? region_s + (uint32_t)l * kStageLevelBytes + o : stage_s + o;
-    const float* src = xr + (size_t)p.layer_sub[tr.layer0 + l] * SS;
+    const float* src = xr + (size_t)p.lsub[tr.layer0 + l] * SS;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
   }
 }
@@ -429,10 +429,10 @@ __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const
       const float* xr = p.queries + (size_t)q * d + j;
       const float* cr = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + j : nullptr;
 #pragma unroll
-      for (int l = 0; l < MT; ++l) v[l] = __ldg(xr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
+      for (int l = 0; l < MT; ++l) v[l] = __ldg(xr + (size_t)p.lsub[tr.layer0 + l] * SS);
       if (cr) {
 #pragma unroll
-        for (int l = 0; l < MT; ++l) v[l] -= __ldg(cr + (size_t)p.layer_sub[tr.layer0 + l] * SS);
+        for (int l = 0; l < MT; ++l) v[l] -= __ldg(cr + (size_t)p.lsub[tr.layer0 + l] * SS);
       }
       const uint32_t o = (uint32_t)(i >> 1) * pair_bytes + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
 #pragma unroll
@@ -447,7 +447,7 @@ __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const
   const bool active = kb * 32 < K;                   // K < 256: idle codeword blocks
   const uint32_t dsm_s = smem_u32(et_dsm);
   auto load_cw = [&](int l, float (&c)[SS]) {
-    const int m = p.layer_sub[tr.layer0 + l];
+    const int m = p.lsub[tr.layer0 + l];
     const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
 #pragma unroll
     for (int j = 0; j < SS; j += 4) {
@@ -558,7 +558,7 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
     for (int item = warp; item < MT * nb; item += kWarps) {
       const int l = item / nb, kb = item - l * nb;
       const int k = kb * 32 + lane;
-      const int m = p.layer_sub[tr.layer0 + l];
+      const int m = p.lsub[tr.layer0 + l];
       for (int i = 0; i < nq; ++i) {
         const float v = (k < K) ? __ldg(p.luts + ((size_t)sm.qidx[i] * p.M + m) * K + k) : 0.f;
         if (k < K) *tab_slot(sm, lut0, l, lv0, k, i) = v;
@@ -578,7 +578,7 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
     const int l = pass / npl, jc = pass - l * npl;
     const int j = jc * DC + sj;
     if (sq < 0 || j >= s) return 0.f;
-    const int m = p.layer_sub[tr.layer0 + l];
+    const int m = p.lsub[tr.layer0 + l];
     float v = __ldg(p.queries + (size_t)sq * d + (size_t)m * s + j);
     if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * s + j);
     return v;
@@ -590,7 +590,7 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
     const int l = pass / npl, jc = pass - l * npl;
     const int j0 = jc * DC;
     const int nj = min(DC, s - j0);
-    const int m = p.layer_sub[tr.layer0 + l];
+    const int m = p.lsub[tr.layer0 + l];
     const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s + j0;
     if (p.vec4 && (s & 3) == 0) {   // 16-byte aligned rows: float4 loads
 #pragma unroll
