@@ -1217,6 +1217,46 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
         if (keep) base[n + __popc(m & ((1u << lane) - 1u))] = v;
         n += __popc(m);
       }
+      // exact unit-level top-k of the merged list (it fits the warp's registers):
+      // at most ~k survivors per unit and a tight per-query bound for the
+      // other units and the finalize prefilter
+      constexpr int kCap = kRefreshPer * 32;
+      bool tightened = false;
+      while (n > kCap) {
+        // longer lists: the exact k-th of the first kCap entries bounds the
+        // query's k-th distance; filter the rest by it (in place) and repeat
+        __syncwarp();
+        int nc;
+        float nt;
+        refresh_buffer(base, kCap, p.k, p.group_mult, p.group_minid, &nc, &nt);
+        const uint32_t ntb = __float_as_uint(nt);
+        int m = nc;
+        for (int i0 = kCap; i0 < n; i0 += 32) {
+          const int idx = i0 + lane;
+          uint2 v = make_uint2(0xffffffffu, 0);
+          if (idx < n) v = base[idx];
+          const bool keep = (idx < n) && v.x <= ntb;
+          const unsigned mk = __ballot_sync(FULLMASK, keep);
+          __syncwarp();
+          if (keep) base[m + __popc(mk & ((1u << lane) - 1u))] = v;
+          m += __popc(mk);
+        }
+        __syncwarp();
+        tb = min(tb, ntb);
+        tightened = true;
+        if (m >= n) break;   // no progress (ties): leave the list as it is
+        n = m;
+      }
+      if (n > p.k && n <= kCap) {
+        __syncwarp();
+        int nc;
+        float nt;
+        refresh_buffer(base, n, p.k, p.group_mult, p.group_minid, &nc, &nt);
+        n = nc;
+        tb = min(tb, __float_as_uint(nt));
+        tightened = true;
+      }
+      if (tightened && p.qthr && lane == 0 && sm.qidx[L] >= 0) atomicMin(p.qthr + sm.qidx[L], tb);
       if (lane < kWarps) p.cand_cnt[((size_t)unit * 32 + L) * kWarps + lane] = (lane == 0) ? n : 0;
       if (lane == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + L] = __uint_as_float(tb);
     }
