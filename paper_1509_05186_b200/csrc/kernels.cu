@@ -967,7 +967,9 @@ __device__ __forceinline__ void share_threshold(EmitCtx& e, const SmemScan& sm) 
 // from the per-tree partials of its leaves (written by the trees' scans).
 // Tuples [ga, gb) of this warp, 32 at a time: their leaves and multiplicities
 // in one coalesced load each, then the per-query partials (coalesced across
-// lanes) eight tuples at a time.
+// lanes) kJoinBatch tuples at a time.
+constexpr int kJoinBatch = 16;   // tuples whose partials are in flight at once
+
 __device__ void join_tuples(EmitCtx& e, const SmemScan& sm, uint32_t ga, uint32_t gb) {
   const ScanParams& p = *e.p;
   const int lane = lane_id();
@@ -978,28 +980,28 @@ __device__ void join_tuples(EmitCtx& e, const SmemScan& sm, uint32_t ga, uint32_
 #pragma unroll
     for (int t = 0; t < kMaxTrees; ++t) my_l[t] = (t < p.T && lane < n) ? __ldg(p.tup_leaf[t] + g0 + lane) : 0u;
     const uint32_t my_mu = (topk && lane < n) ? __ldg(p.group_mult + g0 + lane) : 0u;
-    for (int u0 = 0; u0 < n; u0 += 8) {
-      float acc[8];
+    for (int u0 = 0; u0 < n; u0 += kJoinBatch) {
+      float acc[kJoinBatch];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kJoinBatch; ++u) {
         const uint32_t l0 = __shfl_sync(FULLMASK, my_l[0], u0 + u);
         acc[u] = (u0 + u < n) ? e.part[(size_t)p.part_base[0] + (size_t)l0 * 32 + lane] : 0.f;
       }
 #pragma unroll
       for (int t = 1; t < kMaxTrees; ++t) {
         if (t < p.T) {
-          float pv[8];
+          float pv[kJoinBatch];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < kJoinBatch; ++u) {
             const uint32_t lt = __shfl_sync(FULLMASK, my_l[t], u0 + u);
             pv[u] = (u0 + u < n) ? e.part[(size_t)p.part_base[t] + (size_t)lt * 32 + lane] : 0.f;
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc[u] = acc[u] + pv[u];
+          for (int u = 0; u < kJoinBatch; ++u) acc[u] = acc[u] + pv[u];
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kJoinBatch; ++u) {
         const uint32_t mult = __shfl_sync(FULLMASK, my_mu, u0 + u);
         if (u0 + u < n) emit_group(e, acc[u], g0 + u0 + u, mult);
       }
