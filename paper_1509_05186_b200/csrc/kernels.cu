@@ -536,6 +536,88 @@ __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const
   if constexpr (MT == 8) tmem_fence_after();         // TMEM level 0 visible to the scan's tcgen05.ld
 }
 
+// Few queries with long sub-vectors (c3: s = 60, <= 8 queries per CTA): one
+// staging pass per level (the small stage holds 8 queries x 64 dims), each
+// warp owns codeword block kb = w & 7 and the queries g, g+2, g+4, g+6
+// (g = w >> 3) and runs the whole j-ascending FMA chain of each entry in
+// registers over 16-dimension codeword chunks (next chunk prefetched) -- two
+// barriers per level instead of two per 16-dimension pass.
+template <int SS>
+__device__ void build_tables_wide(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq, int cell) {
+  static_assert(SS > kDC && SS <= 64 && SS % 4 == 0, "wide staging: 16 < s <= 64, s % 4 == 0");
+  constexpr int NCH = (SS + kDC - 1) / kDC;
+  const TreeDev& tr = p.tree[t];
+  const int MT = tr.MT;
+  const int lv0 = (MT == 8) ? 1 : 0;
+  const int K = p.K, d = p.d;
+  const int lane = lane_id(), warp = warp_id();
+  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
+  const int kb = warp & 7, g = warp >> 3;
+  const int k = kb * 32 + lane;
+  const bool kvalid = k < K;
+  const int si = threadIdx.x >> 6, sj = threadIdx.x & 63;   // staging element (8 x 64)
+  const int sq = (si < nq) ? sm.qidx[si] : -1;
+  auto fetch = [&](int l) -> float {
+    if (sq < 0 || sj >= SS) return 0.f;
+    const int m = p.lsub[tr.layer0 + l];
+    float v = __ldg(p.queries + (size_t)sq * d + (size_t)m * SS + sj);
+    if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * SS + sj);
+    return v;
+  };
+  float nxt = fetch(0);
+  __syncthreads();                              // previous users of the stage are done
+  sm.stage[threadIdx.x] = nxt;
+  __syncthreads();
+  for (int l = 0; l < MT; ++l) {
+    if (l + 1 < MT) nxt = fetch(l + 1);         // next level's stage value
+    const int m = p.lsub[tr.layer0 + l];
+    const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float c[kDC], cn[kDC];
+#pragma unroll
+    for (int j = 0; j < kDC; j += 4) {
+      const float4 v = (j < SS) ? __ldg(reinterpret_cast<const float4*>(crow + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
+    }
+#pragma unroll
+    for (int jc = 0; jc < NCH; ++jc) {
+      if (jc + 1 < NCH) {
+#pragma unroll
+        for (int j = 0; j < kDC; j += 4) {
+          const int jj = (jc + 1) * kDC + j;
+          const float4 v = (jj < SS) ? __ldg(reinterpret_cast<const float4*>(crow + jj)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          cn[j] = v.x; cn[j + 1] = v.y; cn[j + 2] = v.z; cn[j + 3] = v.w;
+        }
+      }
+      constexpr int NJ0 = SS - (NCH - 1) * kDC;   // size of the last chunk
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const int i = g + 2 * qq;
+        if (i < nq) {
+          const float* x = sm.stage + i * 64 + jc * kDC;
+#pragma unroll
+          for (int j = 0; j < kDC; ++j) {
+            if (jc < NCH - 1 || j < NJ0) {
+              const float tt = x[j] - c[j];
+              acc[qq] = fmaf(tt, tt, acc[qq]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kDC; ++j) c[j] = cn[j];
+    }
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const int i = g + 2 * qq;
+      if (i < nq && kvalid) *tab_slot(sm, lut0, l, lv0, k, i) = acc[qq];
+    }
+    __syncthreads();
+    if (l + 1 < MT) sm.stage[threadIdx.x] = nxt;
+    __syncthreads();
+  }
+}
+
 // Build the tables of tree t for this CTA's queries (fused).
 // Passes over (level, 16-dimension chunk): the chunk of the active queries'
 // sub-vectors (minus the coarse centroid for IVF residuals) is staged in shared
@@ -1134,7 +1216,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
         phase_mark(unit, 2);
       }
     } else {
-      build_tables<SS>(p, sm, t, unit, nq, cell);
+      if constexpr (SS > kDC && SS <= 64 && SS % 4 == 0) {
+        if (nq <= 8 && !p.luts && p.vec4) build_tables_wide<SS>(p, sm, t, unit, nq, cell);
+        else build_tables<SS>(p, sm, t, unit, nq, cell);
+      } else {
+        build_tables<SS>(p, sm, t, unit, nq, cell);
+      }
       __syncthreads();
     }
     if (tr.MT == 8 && !level0_done) {   // level 0 -> TMEM (every warp copies a quarter of its quadrant's columns)
