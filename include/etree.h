@@ -178,7 +178,13 @@ et_status et_etree_distances(const et_index* index, const float* codebooks,
 
 /* Fused top-k (north_star item 4): for each query the k smallest
  * (distance, id) pairs; dist: DEVICE fp32 [Q][k]; ids: DEVICE int32 [Q][k].
- * 1 <= k <= 256.  Tables as for et_etree_distances. */
+ * 1 <= k <= 256.  Tables as for et_etree_distances.  Launches:
+ * a memset of the per-query thresholds, the scan kernel (fused tables +
+ * Distance-Context scan + candidates; for forests the per-tree partials and
+ * the tuple join), and the finalize kernel.  `workspace` (DEVICE, caller-owned,
+ * et_workspace_size bytes) must not be shared by calls in flight at the same
+ * time.  Errors: ET_ERR_CONFIG (null output, k out of range, IVF index, Q < 0),
+ * ET_ERR_WORKSPACE (too small), ET_ERR_CUDA (launch failure). */
 et_status et_etree_topk(const et_index* index, const float* codebooks, int32_t d,
                         const float* luts, const float* queries, int64_t Q,
                         int32_t k, float* dist, int32_t* ids, void* workspace,
