@@ -256,21 +256,25 @@ def roofline(cfg, stats, kern_ms, peaks, clock_mhz, Q, n_tables=None, lookups=No
     return out
 
 
-def north_star_roofline(cfg, stats, step_ms, peaks, Q):
+def north_star_roofline(cfg, stats, step_ms, peaks, Q, n_tables=None, lookups=None):
     """BASELINE north_star's narrow roofline: max(tree bytes / HBM, lookups /
-    shared-memory rate) and the complete one (+ tables built + top-k output)."""
+    shared-memory rate) and the complete one (+ tables built + output).
+    IVF: n_tables = Q * nprobe residual tables, lookups over the probed lists
+    only (passed in); full output (topk == 0): the Q x N fp32 matrix."""
     hbm = float(peaks.get("hbm_gbs", 6558.1)) * 1e9
     clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     smem_rate = 148 * 32 * clk                       # conflict-free 4-byte lookups / s
     alu = 148 * 128 * clk
-    lookups = sum(s["lookups"] for s in stats) * Q
-    if len(stats) > 1:
-        lookups += stats[0]["groups"] * Q             # one join add per tuple
+    n_tables = Q if n_tables is None else n_tables
+    if lookups is None:
+        lookups = sum(s["lookups"] for s in stats) * Q
+        if len(stats) > 1:
+            lookups += stats[0]["groups"] * Q         # one join add per tuple
     tree_bytes = sum(s["device_bytes"] for s in stats)
     t_tree = tree_bytes / hbm
     t_smem = lookups / smem_rate
-    t_lut_build = 2.0 * Q * cfg.K * cfg.d / alu
-    t_out = Q * cfg.topk * 8 / hbm
+    t_lut_build = 2.0 * n_tables * cfg.K * cfg.d / alu
+    t_out = (Q * cfg.N * 4 if cfg.topk == 0 else Q * cfg.topk * 8) / hbm
     narrow = max(t_tree, t_smem)
     complete = max(t_tree + t_out, t_smem, t_lut_build)
     s = step_ms / 1e3
@@ -278,7 +282,7 @@ def north_star_roofline(cfg, stats, step_ms, peaks, Q):
             "frac_narrow": round(narrow / s, 4), "frac_complete": round(complete / s, 4),
             "terms_us": {"tree_bytes": round(t_tree * 1e6, 3), "smem_lookups": round(t_smem * 1e6, 3),
                          "table_build_alu": round(t_lut_build * 1e6, 3), "topk_out": round(t_out * 1e6, 3)},
-            "lookups_per_query": lookups // Q, "tree_bytes": tree_bytes}
+            "lookups_per_query": int(lookups // Q), "tree_bytes": tree_bytes}
 
 
 def cpu_baseline(cfg, cb, codes, qx, budget_s=15.0):
@@ -489,7 +493,9 @@ def run_ours(args):
                        "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
                        "timing": "CUDA graph replay of one step, CUDA events per step" if world == 1 else "CUDA events per step"},
             "roofline": roof,
-            "north_star_roofline": north_star_roofline(cfg, stats, step_ms, peaks, Q),
+            "north_star_roofline": north_star_roofline(cfg, stats, step_ms, peaks, Q,
+                                                       Q * cfg.ivf_nprobe if ivf else None,
+                                                       stats[0]["lookups"] / max(1, cfg.N) * pairs if ivf else None),
             "kernels_ms": {k_: round(v, 5) for k_, v in kern.items()},
             "dominant_kernel": dom,
             "e2e": {"value": pairs / (e2e_ms / 1e3), "unit": UNIT,
