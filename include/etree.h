@@ -137,7 +137,8 @@ et_status et_build_flat(const uint8_t* codes, const int32_t* ids, int64_t n,
 /* IVF index: one E-Tree per inverted list.  codes: residual codes
  * HOST [n][M]; list_of: HOST int32 [n] list of each vector (0..nlist-1);
  * coarse: HOST fp32 [nlist][d] (uploaded; used for residual tables);
- * codebooks: HOST fp32 [M][K][d/M] residual codebook (uploaded). */
+ * codebooks: HOST fp32 [M][K][d/M] residual codebook (uploaded).
+ * Errors: ET_ERR_INVALID_VECTOR for a non-finite centroid or codeword. */
 et_status et_build_ivf(const uint8_t* codes, const int32_t* ids, int64_t n,
                        int32_t M, int32_t K, const int32_t* list_of,
                        int32_t nlist, const float* coarse, int32_t d,
@@ -192,7 +193,11 @@ et_status et_etree_topk(const et_index* index, const float* codebooks, int32_t d
 
 /* IVF search: probe the nprobe nearest coarse cells (fp32 direct difference,
  * ties -> lower cell), residual tables per (query, cell), per-list E-Tree
- * scan, fused top-k.  probes: optional DEVICE int32 [Q][nprobe] output. */
+ * scan, fused top-k.  probes: optional DEVICE int32 [Q][nprobe] output.
+ * Queries are not checked on the host (they are device data, the call is
+ * async): a non-finite query's coarse distances are treated as +inf, so its
+ * probes are the lowest cell indices and its distances +inf/NaN -- defined,
+ * never an out-of-bounds access. */
 et_status et_ivf_topk(const et_index* index, const float* queries, int64_t Q,
                       int32_t nprobe, int32_t k, float* dist, int32_t* ids,
                       int32_t* probes, void* workspace, size_t workspace_bytes,

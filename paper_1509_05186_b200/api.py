@@ -42,8 +42,9 @@ def _stream(stream=None) -> Optional[int]:
 
 
 def _dev(x, dtype):
-    torch = _t()
-    assert x.is_cuda and x.is_contiguous() and x.dtype == dtype, (x.device, x.dtype, x.is_contiguous())
+    if not (x.is_cuda and x.is_contiguous() and x.dtype == dtype):
+        raise ValueError(f"expected a contiguous CUDA {dtype} tensor, got {x.dtype} on {x.device} "
+                         f"(contiguous={x.is_contiguous()})")
     return x
 
 
@@ -86,7 +87,7 @@ class Index:
                                         C.byref(G), C.byref(nl)))
         self.T, self.N, self.M, self.K = T.value, n.value, M.value, K.value
         self.groups, self.nlist = G.value, nl.value
-        self._ws = None
+        self._ws = {}   # one workspace per (device, stream): a call in flight owns its workspace
 
     # ---------------------------------------------------------------- builds
     @staticmethod
@@ -159,11 +160,22 @@ class Index:
         check(_lib.load().et_workspace_size(self._h, Q, k, nprobe, C.byref(b)))
         return b.value
 
-    def _workspace(self, nbytes: int, device):
+    def _workspace(self, nbytes: int, device, stream=None):
+        """Workspace for a call on ``stream`` (etree.h: one workspace per call
+        in flight).  Cached per (device, stream); when it grows, the old block
+        is released with record_stream so the caching allocator cannot hand
+        it out while a kernel on that stream may still read it."""
         torch = _t()
-        if self._ws is None or self._ws.numel() < nbytes or self._ws.device != device:
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        return self._ws
+        s = torch.cuda.current_stream(device) if stream is None else stream
+        key = (device, s.cuda_stream)
+        ws = self._ws.get(key)
+        if ws is None or ws.numel() < nbytes:
+            if ws is not None:
+                ws.record_stream(s)
+            with torch.cuda.stream(s):
+                ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self._ws[key] = ws
+        return ws
 
     # ---------------------------------------------------------------- queries
     def et_etree_topk(self, k: int, queries=None, codebooks=None, luts=None, out=None, stream=None):
@@ -183,7 +195,7 @@ class Index:
         else:
             dist, ids = out
         nb = self.et_workspace_size(Q, k)
-        ws = self._workspace(nb, ref.device)
+        ws = self._workspace(nb, ref.device, stream)
         check(_lib.load().et_etree_topk(self._h, _ptr(codebooks), d, _ptr(luts), _ptr(queries), Q, k,
                                         _ptr(dist), _ptr(ids), _ptr(ws), ws.numel(), _stream(stream)))
         return dist, ids
@@ -197,7 +209,7 @@ class Index:
         if out is None:
             out = torch.empty((Q, self.N), dtype=torch.float32, device=ref.device)
         nb = self.et_workspace_size(Q, 0)
-        ws = self._workspace(nb, ref.device)
+        ws = self._workspace(nb, ref.device, stream)
         check(_lib.load().et_etree_distances(self._h, _ptr(codebooks), d, _ptr(luts), _ptr(queries), Q,
                                              _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
         return out
@@ -210,7 +222,7 @@ class Index:
         ids = torch.empty((Q, k), dtype=torch.int32, device=queries.device)
         probes = torch.empty((Q, nprobe), dtype=torch.int32, device=queries.device)
         nb = self.et_workspace_size(Q, k, nprobe)
-        ws = self._workspace(nb, queries.device)
+        ws = self._workspace(nb, queries.device, stream)
         check(_lib.load().et_ivf_topk(self._h, _ptr(queries), Q, nprobe, k, _ptr(dist), _ptr(ids),
                                       _ptr(probes), _ptr(ws), ws.numel(), _stream(stream)))
         return (dist, ids, probes) if return_probes else (dist, ids)
@@ -287,13 +299,26 @@ def et_build_coarse(train, nlist: int, lloyd_iters: int, seed: int):
 
 
 def et_merge_topk(dist, ids, stream=None):
-    """dist/ids [G, Q, k] (e.g. all-gathered shards) -> merged [Q, k]."""
+    """dist/ids [G, Q, k] (e.g. all-gathered shards) -> merged [Q, k].
+
+    float32 distances and int32 ids on one CUDA device; non-contiguous inputs
+    are copied to locals that stay alive until the launch has been enqueued
+    on ``stream`` (the caching allocator then orders any reuse after it)."""
     torch = _t()
-    G, Q, k = dist.shape
-    od = torch.empty((Q, k), dtype=torch.float32, device=dist.device)
-    oi = torch.empty((Q, k), dtype=torch.int32, device=dist.device)
-    check(_lib.load().et_merge_topk(_ptr(dist.contiguous()), _ptr(ids.contiguous()), G, Q, k,
-                                    _ptr(od), _ptr(oi), _stream(stream)))
+    if dist.dim() != 3 or ids.shape != dist.shape:
+        raise ValueError(f"et_merge_topk: need dist/ids of equal shape [G, Q, k], got {tuple(dist.shape)} / {tuple(ids.shape)}")
+    if dist.device != ids.device or not dist.is_cuda:
+        raise ValueError("et_merge_topk: dist and ids must be on the same CUDA device")
+    dc = _dev(dist.contiguous(), torch.float32)
+    ic = _dev(ids.contiguous(), torch.int32)
+    G, Q, k = dc.shape
+    od = torch.empty((Q, k), dtype=torch.float32, device=dc.device)
+    oi = torch.empty((Q, k), dtype=torch.int32, device=dc.device)
+    st = _stream(stream)
+    check(_lib.load().et_merge_topk(_ptr(dc), _ptr(ic), G, Q, k, _ptr(od), _ptr(oi), st))
+    if stream is not None:   # temporaries used on a side stream: keep them alive there
+        dc.record_stream(stream)
+        ic.record_stream(stream)
     return od, oi
 
 

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(OUT_DIR, "libetree.so")
-SOURCES = ["kernels.cu", "host.cpp"]
+SOURCES = ["scan_s16.cu", "scan_s60.cu", "scan_s0.cu", "kernels.cu", "host.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -34,17 +34,20 @@ def build(force: bool = False, verbose: bool = False, out_dir: str = OUT_DIR, de
     if out_dir == OUT_DIR and not defines and not force and not _stale():
         return LIB
     os.makedirs(out_dir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    dflags = [f"-D{d}" for d in defines]
+    for src in SOURCES:   # one nvcc per translation unit, in parallel
         obj = os.path.join(out_dir, src.rsplit(".", 1)[0] + ".o")
-        dflags = [f"-D{d}" for d in defines]
         cmd = [NVCC, *FLAGS, *dflags, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, *FLAGS, *dflags, "-x", "cu", "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        procs.append((src, subprocess.Popen(cmd)))
         objs.append(obj)
+    failed = [src for src, pr in procs if pr.wait() != 0]
+    if failed:
+        raise RuntimeError(f"nvcc failed for {failed}")
     tmp = lib + ".tmp"
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
                     "-Xlinker", "-z,defs", "-lpthread"], check=True)

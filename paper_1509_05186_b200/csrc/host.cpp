@@ -475,6 +475,10 @@ static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t 
   check_ids(ids, n);
   for (int64_t i = 0; i < n; ++i)
     if (list_of[i] < 0 || list_of[i] >= nlist) fail(ET_ERR_CONFIG, "list_of out of range");
+  for (int64_t i = 0; i < (int64_t)nlist * d; ++i)
+    if (!std::isfinite(coarse[i])) fail(ET_ERR_INVALID_VECTOR, "non-finite coarse centroid");
+  for (int64_t i = 0; i < (int64_t)M * K * (d / M); ++i)
+    if (!std::isfinite(codebooks[i])) fail(ET_ERR_INVALID_VECTOR, "non-finite residual codebook");
   std::unique_ptr<et_index> ix(new et_index);
   ix->kind = kIvf;
   ix->N = n; ix->M = M; ix->K = K; ix->T = 1; ix->d = d; ix->nlist = nlist;
@@ -949,17 +953,10 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   // register fast path when groups are large (few candidates per query)
   fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
   sp.compact = !fp.fast;
-  // Finalize inside the scan kernel (pl.S == 1 && fp.fast) is exact too, but its
-  // latency-bound tail runs with the SM otherwise idle (measured +30 us on c2):
-  // the separate high-occupancy kernel wins, so the fused path stays off.
-  if (false && pl.S == 1 && fp.fast) {
-    sp.fuse_fin = 1;
-    sp.fin = fp;
-    cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
-  } else {
-    cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
-    cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
-  }
+  // (a finalize fused into the scan kernel was measured +30 us on c2: its
+  // latency-bound tail runs with the SM otherwise idle)
+  cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
+  cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
   ET_API_END
 }
 

@@ -98,13 +98,10 @@ struct ScanParams {
   unsigned* qthr = nullptr;           // [Q] per-query threshold (float bits), shared by all units
   int qthr_shared = 0;                // several units per query (S > 1, IVF): share during the scan
   int vec4 = 1;                       // query/codebook rows 16-byte aligned
-  int fuse_fin = 0;                   // S == 1: finalize this CTA's queries in the scan kernel
   int compact = 0;                    // merge each lane's 16 per-warp lists at the end (long lists)
-  FinParams fin;
 };
 
 // ---- launchers (kernels.cu); each returns cudaGetLastError() ----
-size_t scan_smem_bytes(int MTmax);
 cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st);
 cudaError_t launch_finalize(const FinParams& p, cudaStream_t st);
 cudaError_t launch_fill_flat(int64_t Q, int n_chunks, int* chunk_q, int* qslot_off, int* qslot,

@@ -13,1388 +13,27 @@
 //
 // Design notes are in DESIGN.md §4-5; every floating-point table entry is the
 // direct difference sum_j (x_j - c_j)^2 accumulated in fp32 with j ascending.
-#include "internal.h"
-
-#include <cfloat>
-#include <climits>
-#include <cstdint>
-#include <algorithm>
+#include "common.cuh"
 
 namespace et {
 
-#define FULLMASK 0xffffffffu
+cudaError_t launch_scan_16(const ScanParams& p, size_t smem, cudaStream_t st);
+cudaError_t launch_scan_60(const ScanParams& p, size_t smem, cudaStream_t st);
+cudaError_t launch_scan_0(const ScanParams& p, size_t smem, cudaStream_t st);
 
-__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
-__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
-
-// Optional per-CTA phase timestamps (experiment builds: -DET_PHASE_TIMING).
-#ifdef ET_PHASE_TIMING
-__device__ unsigned long long g_phase[1 << 16][8];
-__device__ __forceinline__ void phase_mark(int unit, int i) {
-  if (threadIdx.x == 0 && unit < (1 << 16)) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_phase[unit][i] = t;
-  }
-}
-#else
-__device__ __forceinline__ void phase_mark(int, int) {}
-#endif
-
-// ---------------------------------------------------------------------------
-// table build helpers
-// ---------------------------------------------------------------------------
-
-// Swizzled shared-memory table: entry (level, k, lane) of the CTA's 32 queries.
-// A lookup by warp-uniform (level, k) with lane = query touches 32 consecutive
-// words (conflict-free); a build store with lanes = 32 consecutive codewords and
-// a uniform query slot i lands on bank (i ^ lane): also conflict-free.
-__device__ __forceinline__ int tab_index(int lvl, int k, int i) {
-  return ((lvl << 8) + k) * 32 + (i ^ (k & 31));
-}
-
-// Dynamic shared memory of the scan kernel, addressed by byte offset through
-// this extern array so the compiler emits LDS/STS (and may reorder loads).
-extern __shared__ __align__(16) unsigned char et_dsm[];
-__device__ __forceinline__ float4 lds4_off(uint32_t off) {
-  return *reinterpret_cast<const float4*>(et_dsm + off);
-}
-__device__ __forceinline__ void sts_off(uint32_t off, float v) {
-  *reinterpret_cast<float*>(et_dsm + off) = v;
-}
-
-// Explicit shared-memory accesses (32-bit shared addresses; avoids generic
-// addressing in the hot loops).
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ float lds(uint32_t a) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ float4 lds4(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-  return v;
-}
-// predicated load: v is returned unchanged when !pred (no shared-memory traffic)
-__device__ __forceinline__ float lds_if(uint32_t a, bool pred, float v) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
-               : "+f"(v) : "r"(a), "r"((int)pred));
-  return v;
-}
-// predicated load; the result is undefined when !pred (callers never use it then)
-__device__ __forceinline__ float lds_if_w(uint32_t a, bool pred) {
-  float v;
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
-               : "=f"(v) : "r"(a), "r"((int)pred));
-  return v;
-}
-__device__ __forceinline__ void sts(uint32_t a, float v) {
-  asm volatile("st.shared.f32 [%0], %1;" :: "r"(a), "f"(v) : "memory");
-}
-// byte address of table entry (level, k, lane): see tab_index
-__device__ __forceinline__ uint32_t tab_addr(uint32_t tab_s, int lvl, uint32_t k, uint32_t lane4) {
-  return tab_s + ((uint32_t)lvl << 15) + (k << 7) + ((lane4 ^ (k << 2)) & 0x7cu);
-}
-
-// Squared distance between the query sub-vector x[0..s) (optionally minus the
-// coarse centroid cc) and codeword c (registers), fp32, j ascending, FMA.
-template <int SS>
-struct Codeword {
-  float c[SS];
-  __device__ __forceinline__ void load(const float* row) {
-#pragma unroll
-    for (int j = 0; j < SS; j += 4) {
-      float4 v = __ldg(reinterpret_cast<const float4*>(row + j));
-      c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
-    }
-  }
-};
-
-// Computes table entries for queries slots [0, nq) and codeword `crow` (one per
-// lane).  `xq(i)` returns the pointer to slot i's sub-vector; `cc` is the coarse
-// centroid sub-vector (IVF) or null.  `store(i, v)` writes the entry.
-template <int SS, class XQ, class ST>
-__device__ __forceinline__ void entries_fixed(const float* crow, bool kvalid, int nq,
-                                              XQ xq, const float* cc, ST store) {
-  Codeword<SS> cw;
-  if (kvalid) cw.load(crow);
-  else {
-#pragma unroll
-    for (int j = 0; j < SS; ++j) cw.c[j] = 0.f;
-  }
-  int i = 0;
-  for (; i + 4 <= nq; i += 4) {
-    const float4* x0 = reinterpret_cast<const float4*>(xq(i));
-    const float4* x1 = reinterpret_cast<const float4*>(xq(i + 1));
-    const float4* x2 = reinterpret_cast<const float4*>(xq(i + 2));
-    const float4* x3 = reinterpret_cast<const float4*>(xq(i + 3));
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-    for (int jb = 0; jb < SS / 4; ++jb) {
-      float4 v0 = __ldg(x0 + jb), v1 = __ldg(x1 + jb), v2 = __ldg(x2 + jb), v3 = __ldg(x3 + jb);
-      if (cc) {
-        float4 cv = __ldg(reinterpret_cast<const float4*>(cc) + jb);
-        v0.x -= cv.x; v0.y -= cv.y; v0.z -= cv.z; v0.w -= cv.w;
-        v1.x -= cv.x; v1.y -= cv.y; v1.z -= cv.z; v1.w -= cv.w;
-        v2.x -= cv.x; v2.y -= cv.y; v2.z -= cv.z; v2.w -= cv.w;
-        v3.x -= cv.x; v3.y -= cv.y; v3.z -= cv.z; v3.w -= cv.w;
-      }
-      const float* c = cw.c + 4 * jb;
-      float t;
-      t = v0.x - c[0]; a0 = fmaf(t, t, a0); t = v0.y - c[1]; a0 = fmaf(t, t, a0);
-      t = v0.z - c[2]; a0 = fmaf(t, t, a0); t = v0.w - c[3]; a0 = fmaf(t, t, a0);
-      t = v1.x - c[0]; a1 = fmaf(t, t, a1); t = v1.y - c[1]; a1 = fmaf(t, t, a1);
-      t = v1.z - c[2]; a1 = fmaf(t, t, a1); t = v1.w - c[3]; a1 = fmaf(t, t, a1);
-      t = v2.x - c[0]; a2 = fmaf(t, t, a2); t = v2.y - c[1]; a2 = fmaf(t, t, a2);
-      t = v2.z - c[2]; a2 = fmaf(t, t, a2); t = v2.w - c[3]; a2 = fmaf(t, t, a2);
-      t = v3.x - c[0]; a3 = fmaf(t, t, a3); t = v3.y - c[1]; a3 = fmaf(t, t, a3);
-      t = v3.z - c[2]; a3 = fmaf(t, t, a3); t = v3.w - c[3]; a3 = fmaf(t, t, a3);
-    }
-    store(i, a0); store(i + 1, a1); store(i + 2, a2); store(i + 3, a3);
-  }
-  for (; i < nq; ++i) {
-    const float4* x0 = reinterpret_cast<const float4*>(xq(i));
-    float a0 = 0.f;
-#pragma unroll
-    for (int jb = 0; jb < SS / 4; ++jb) {
-      float4 v0 = __ldg(x0 + jb);
-      if (cc) {
-        float4 cv = __ldg(reinterpret_cast<const float4*>(cc) + jb);
-        v0.x -= cv.x; v0.y -= cv.y; v0.z -= cv.z; v0.w -= cv.w;
-      }
-      const float* c = cw.c + 4 * jb;
-      float t;
-      t = v0.x - c[0]; a0 = fmaf(t, t, a0); t = v0.y - c[1]; a0 = fmaf(t, t, a0);
-      t = v0.z - c[2]; a0 = fmaf(t, t, a0); t = v0.w - c[3]; a0 = fmaf(t, t, a0);
-    }
-    store(i, a0);
-  }
-}
-
-// Generic sub-vector length (any s): scalar loads.
-template <class XQ, class ST>
-__device__ __forceinline__ void entries_generic(const float* crow, bool kvalid, int s, int nq,
-                                                XQ xq, const float* cc, ST store) {
-  for (int i = 0; i < nq; ++i) {
-    const float* x = xq(i);
-    float a = 0.f;
-    for (int j = 0; j < s; ++j) {
-      float xv = __ldg(x + j);
-      if (cc) xv -= __ldg(cc + j);
-      float t = xv - (kvalid ? __ldg(crow + j) : 0.f);
-      a = fmaf(t, t, a);
-    }
-    store(i, a);
-  }
-}
-
-template <int SS, class XQ, class ST>
-__device__ __forceinline__ void entries(const float* crow, bool kvalid, int s, int nq, XQ xq,
-                                        const float* cc, ST store) {
-  if constexpr (SS > 0) entries_fixed<SS>(crow, kvalid, nq, xq, cc, store);
-  else entries_generic(crow, kvalid, s, nq, xq, cc, store);
-}
-
-// ---------------------------------------------------------------------------
-// K2: the scan kernel
-// ---------------------------------------------------------------------------
-
-struct SmemScan {
-  float* tab;          // [(levels)][256][32] swizzled
-  unsigned* thr;       // [32] CTA-shared top-k thresholds (float bits)
-  int* qidx;           // [32] query of each lane
-  float* stage;        // [32 queries][kDC dims] query sub-vector chunk (table build)
-  uint32_t* tmem_slot; // TMEM base address written by tcgen05.alloc
-  uint32_t tmem;       // TMEM base (level-0 tables of 8-level trees), 0 if unused
-};
-
-// ---------------------------------------------------------------------------
-// Tensor Memory (TMEM) as a lookup-table store.  An 8-level tree needs 8
-// tables of 32 KB for the CTA's 32 queries but shared memory holds 7; level 0
-// lives in TMEM: 256 columns x 32 lanes (lane = query), one copy per warp
-// quadrant (a warp may only address its own 32 TMEM lanes), read with
-// tcgen05.ld.32x32b.x1 by warp-uniform column = codeword.
-// ---------------------------------------------------------------------------
-constexpr int kTmemCols = 256;
-
-__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(slot);
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(a), "r"(kTmemCols) : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t base) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(base), "r"(kTmemCols) : "memory");
-}
-__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ uint32_t tmem_lane_base(uint32_t base) {
-  return base + ((uint32_t)((threadIdx.x >> 5) & 3) * 32u << 16);   // this warp's 32-lane quadrant
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
-               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-                  "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-                  "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])) : "memory");
-}
-__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
-  uint32_t x;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(x) : "r"(taddr));
-  return x;
-}
-__device__ __forceinline__ void tmem_wait_ld(uint32_t& x) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(x));
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// Copy the level-0 table (global scratch row [256][32], just built by this CTA)
-// into each warp quadrant's TMEM lanes: warp w copies 64 columns for quadrant w&3.
-__device__ void tmem_load_level0(const SmemScan& sm, const float* lut0) {
-  const int lane = lane_id(), warp = warp_id();
-  const int sub = warp >> 2;               // 4 warps per quadrant
-  const uint32_t tb = tmem_lane_base(sm.tmem);
-  for (int c0 = sub * 64; c0 < sub * 64 + 64; c0 += 8) {
-    float v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = lut0[(c0 + j) * 32 + lane];
-    tmem_st8(tb + (uint32_t)c0, v);
-  }
-  tmem_wait_st();
-}
-
-constexpr int kDC = 16;   // query dimensions staged per table-build pass
-constexpr int kFinWarpBytes = 2 * 8 * kTopkMax + 3 * 4 * 512 + 4 * 256 + 16;   // sizeof(FinWarp)
-constexpr int kFinRegion = kWarps * kFinWarpBytes;                             // fused finalize scratch
-
-// Table entry (level l, codeword k, query slot i): level 0 of an 8-level tree
-// lives in the global scratch row lut0 (7 levels fill shared memory).
-__device__ __forceinline__ float* tab_slot(const SmemScan& sm, float* lut0, int l, int lv0, int k, int i) {
-  return (l < lv0) ? lut0 + k * 32 + i : sm.tab + tab_index(l - lv0, k, i);
-}
-
-// Inner loop of one build pass: codeword chunk c[0..NJ) (registers) against
-// query slots i = g, g+G, ... read from the staged chunk (broadcast loads).
-template <int NJ, int DC = kDC>
-__device__ __forceinline__ void build_pass_fixed(const SmemScan& sm, float* lut0, int l, int lv0, int k,
-                                                 bool kvalid, const float* c, int nq, int g, int G,
-                                                 bool first) {
-  int i = g;
-  for (; i + G < nq; i += 2 * G) {   // two independent FMA chains
-    const float* x0 = sm.stage + i * DC;
-    const float* x1 = sm.stage + (i + G) * DC;
-    float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
-    float* o1 = tab_slot(sm, lut0, l, lv0, k, i + G);
-    float a0 = 0.f, a1 = 0.f;
-    if (!first && kvalid) { a0 = *o0; a1 = *o1; }
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      const float t0 = x0[j] - c[j];
-      const float t1 = x1[j] - c[j];
-      a0 = fmaf(t0, t0, a0);
-      a1 = fmaf(t1, t1, a1);
-    }
-    if (kvalid) { *o0 = a0; *o1 = a1; }
-  }
-  if (i < nq) {
-    const float* x0 = sm.stage + i * DC;
-    float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
-    float a0 = (!first && kvalid) ? *o0 : 0.f;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      const float t0 = x0[j] - c[j];
-      a0 = fmaf(t0, t0, a0);
-    }
-    if (kvalid) *o0 = a0;
-  }
-}
-
-__device__ __forceinline__ void build_pass_generic(const SmemScan& sm, float* lut0, int l, int lv0, int k,
-                                                   bool kvalid, const float* c, int nj, int nq, int g, int G,
-                                                   bool first) {
-  for (int i = g; i < nq; i += G) {
-    const float* x0 = sm.stage + i * kDC;
-    float* o0 = tab_slot(sm, lut0, l, lv0, k, i);
-    float a0 = (!first && kvalid) ? *o0 : 0.f;
-    for (int j = 0; j < nj; ++j) {
-      const float t0 = x0[j] - c[j];
-      a0 = fmaf(t0, t0, a0);
-    }
-    if (kvalid) *o0 = a0;
-  }
-}
-
-// Packed fp32x2 arithmetic (sm_100a FADD2 / FFMA2): two independent IEEE fp32
-// operations per instruction, each rounded exactly like the scalar op, so an
-// entry computed two-queries-at-a-time equals the scalar j-ascending chain.
-__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void f2unpack(unsigned long long v, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ unsigned long long f2sub(unsigned long long a, unsigned long long b) {
-  unsigned long long r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ unsigned long long f2sqacc(unsigned long long t, unsigned long long acc) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(t), "l"(acc));
-  return r;
-}
-
-// Copy one table (smem region, swizzled [k][lane ^ (k & 31)]) into every warp
-// quadrant's TMEM lanes: warp w copies 64 columns for quadrant w & 3.
-__device__ __forceinline__ void tmem_load_from_smem(const SmemScan& sm, uint32_t region_s) {
-  const int lane = lane_id(), warp = warp_id();
-  const int sub = warp >> 2;
-  const uint32_t tb = tmem_lane_base(sm.tmem);
-  const uint32_t lane4 = (uint32_t)lane << 2;
-  for (int c0 = sub * 64; c0 < sub * 64 + 64; c0 += 8) {
-    float v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = lds(tab_addr(region_s, 0, (uint32_t)(c0 + j), lane4));
-    tmem_st8(tb + (uint32_t)c0, v);
-  }
-  tmem_wait_st();
-}
-
-// Staging layout of the resident build: level l's query pairs at
-// region + l * kStageLevelBytes (16 pairs x 16 dims x 2 queries), the last
-// level's in the small stage.  Element (slot i, dim j) of a level lives at
-// (i / 2) * 128 + j * 8 + (i % 2) * 4.
-constexpr uint32_t kStageLevelBytes = 16 * 16 * 2 * 4;
-
-// Issued at kernel entry (plain E-Tree tables, no coarse residual): the
-// chunk's query sub-vectors are copied straight into the staging layout with
-// cp.async (no registers held), overlapping the CTA's setup (TMEM allocation,
-// first barrier); the build waits with cp.async.wait_all.  Slots without a
-// query are left unwritten (their entries are never looked up).
-template <int SS, int MT>
-__device__ __forceinline__ void stage_async(const ScanParams& p, int t, int chunk, int nch, uint32_t region_s,
-                                            uint32_t stage_s) {
-  const TreeDev& tr = p.tree[t];
-  const int i = threadIdx.x >> 4, j = threadIdx.x & (SS - 1);
-  int q = -1;
-  if (p.flatQ > 0) {
-    const int64_t s0 = (int64_t)chunk * p.flatQ / nch, s1 = (int64_t)(chunk + 1) * p.flatQ / nch;
-    q = (s0 + i < s1) ? (int)(s0 + i) : -1;
-  } else {
-    q = __ldg(p.chunk_q + (size_t)chunk * 32 + i);
-  }
-  if (q < 0) return;
-  const float* xr = p.queries + (size_t)q * p.d + j;
-  const uint32_t o = (uint32_t)(i >> 1) * 128u + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
-#pragma unroll
-  for (int l = 0; l < MT; ++l) {
-    const uint32_t dst = (l < MT - 1) ? region_s + (uint32_t)l * kStageLevelBytes + o : stage_s + o;
-    const float* src = xr + (size_t)p.lsub[tr.layer0 + l] * SS;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
-  }
-}
-
-// Resident-staging table build for s == 16 (every d = 128 configuration).
-// The active queries' sub-vectors are staged ONCE, as query pairs
-// [level][pair][dim][2], levels 0..MT-2 into the shared-memory region of the
-// tree's last level (built last) and level MT-1 into the small stage.  Warp w
-// owns codeword block kb = (w >> 1) & 7 (lane = codeword) and query-pair half
-// g = w & 1; for each level it keeps its codeword in registers and runs two
-// packed FADD2/FFMA2 chains (two query pairs, four entries) at a time against
-// broadcast LDS.128 loads of the staged pairs.  With 8 levels, level 0 is
-// built first into the region of level 6 and copied to TMEM.
-template <int SS, int MT>
-__device__ __forceinline__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, int t, int unit,
-                                                      int nq, int cell, bool staged) {
-  static_assert(SS == kDC, "resident staging handles s == 16");
-  const TreeDev& tr = p.tree[t];
-  constexpr int lv0 = (MT == 8) ? 1 : 0;   // level 0 of an 8-level tree lives in TMEM
-  const int K = p.K, d = p.d;
-  const int lane = lane_id(), warp = warp_id();
-  const uint32_t tab_s = smem_u32(sm.tab);
-  const uint32_t region_s = tab_s + ((uint32_t)(MT - 1 - lv0) << 15);   // last level's table region
-  const uint32_t stage_s = smem_u32(sm.stage);
-  const int np = (nq + 1) >> 1;                                          // query pairs
-  const uint32_t pair_bytes = SS * 2 * 4;                                // 128 B per (level, pair)
-  if (staged) {
-    asm volatile("cp.async.wait_all;" ::: "memory");   // this thread's stage_async copies landed
-  } else {
-    __syncthreads();                                 // previous tree's scan is done with the tables
-    // thread -> (query slot i, dim j); all loads first, then the stores
-    const int i = threadIdx.x >> 4, j = threadIdx.x & (SS - 1);
-    if (i < nq) {
-      float v[MT];
-      const int q = sm.qidx[i];
-      const float* xr = p.queries + (size_t)q * d + j;
-      const float* cr = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + j : nullptr;
-#pragma unroll
-      for (int l = 0; l < MT; ++l) v[l] = __ldg(xr + (size_t)p.lsub[tr.layer0 + l] * SS);
-      if (cr) {
-#pragma unroll
-        for (int l = 0; l < MT; ++l) v[l] -= __ldg(cr + (size_t)p.lsub[tr.layer0 + l] * SS);
-      }
-      const uint32_t o = (uint32_t)(i >> 1) * pair_bytes + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
-#pragma unroll
-      for (int l = 0; l < MT - 1; ++l) sts(region_s + (uint32_t)l * kStageLevelBytes + o, v[l]);
-      sts(stage_s + o, v[MT - 1]);
-    }
-  }
-  const int kb = (warp >> 1) & 7, g = warp & 1;
-  const int k = kb * 32 + lane;
-  const bool kvalid = k < K;
-  const int p0 = g ? (np + 1) >> 1 : 0, p1 = g ? np : (np + 1) >> 1;
-  const bool active = kb * 32 < K;                   // K < 256: idle codeword blocks
-  const uint32_t dsm_s = smem_u32(et_dsm);
-  auto load_cw = [&](int l, float (&c)[SS]) {
-    const int m = p.lsub[tr.layer0 + l];
-    const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
-#pragma unroll
-    for (int j = 0; j < SS; j += 4) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(crow + j));
-      c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
-    }
-  };
-  // Entries of one table (region dst_s) for this warp's query pairs [p0, p1)
-  // of stage xs_s, two pairs (four entries) per iteration.  Every lane writes
-  // all query slots of its codeword's row: slots >= nq are never looked up
-  // (and rows k >= K never addressed), so no store is predicated.
-  auto item = [&](uint32_t dst_s, uint32_t xs_s, const float (&c)[SS]) {
-    const uint32_t drow = dst_s - dsm_s + ((uint32_t)k << 7);   // this lane's row (byte offset)
-    const uint32_t kk = (uint32_t)k << 2;
-    uint32_t xo = xs_s - dsm_s + (uint32_t)p0 * pair_bytes;
-    uint32_t i4 = (uint32_t)p0 << 3;                             // 4 * (first query of the pair)
-    int pi = p0;
-    for (; pi + 1 < p1; pi += 2, xo += 2 * pair_bytes, i4 += 16) {
-      unsigned long long a0 = 0ull, a1 = 0ull;
-#pragma unroll
-      for (int j = 0; j < SS; j += 2) {
-        const float4 u0 = lds4_off(xo + (uint32_t)j * 8u), u1 = lds4_off(xo + pair_bytes + (uint32_t)j * 8u);
-        const unsigned long long cj = f2pack(c[j], c[j]), cj1 = f2pack(c[j + 1], c[j + 1]);
-        unsigned long long t0 = f2sub(f2pack(u0.x, u0.y), cj), t1 = f2sub(f2pack(u1.x, u1.y), cj);
-        a0 = f2sqacc(t0, a0); a1 = f2sqacc(t1, a1);
-        t0 = f2sub(f2pack(u0.z, u0.w), cj1); t1 = f2sub(f2pack(u1.z, u1.w), cj1);
-        a0 = f2sqacc(t0, a0); a1 = f2sqacc(t1, a1);
-      }
-      float e0, o0, e1, o1;
-      f2unpack(a0, e0, o0);
-      f2unpack(a1, e1, o1);
-      sts_off(drow + ((i4 ^ kk) & 0x7cu), e0);
-      sts_off(drow + (((i4 + 4) ^ kk) & 0x7cu), o0);
-      sts_off(drow + (((i4 + 8) ^ kk) & 0x7cu), e1);
-      sts_off(drow + (((i4 + 12) ^ kk) & 0x7cu), o1);
-    }
-    if (pi < p1) {
-      unsigned long long a0 = 0ull;
-#pragma unroll
-      for (int j = 0; j < SS; j += 2) {
-        const float4 u0 = lds4_off(xo + (uint32_t)j * 8u);
-        a0 = f2sqacc(f2sub(f2pack(u0.x, u0.y), f2pack(c[j], c[j])), a0);
-        a0 = f2sqacc(f2sub(f2pack(u0.z, u0.w), f2pack(c[j + 1], c[j + 1])), a0);
-      }
-      float e0, o0;
-      f2unpack(a0, e0, o0);
-      sts_off(drow + ((i4 ^ kk) & 0x7cu), e0);
-      sts_off(drow + (((i4 + 4) ^ kk) & 0x7cu), o0);
-    }
-  };
-  float cw[SS], cwn[SS];
-  if (active) load_cw(0, cw);
-  __syncthreads();                                   // stage complete
-  phase_mark(unit, 5);
-  if constexpr (MT == 8) {
-    // level 0 -> region of level 6 (free until level 6 is built) -> TMEM
-    const uint32_t l0_s = tab_s + (5u << 15);
-    if (active) {
-      load_cw(1, cwn);
-      item(l0_s, region_s, cw);
-#pragma unroll
-      for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
-    }
-    __syncthreads();
-    tmem_fence_after();
-    tmem_load_from_smem(sm, l0_s);   // overlaps the other warps' level-1.. builds
-    tmem_fence_before();
-    phase_mark(unit, 6);
-  }
-  // levels lv0 .. MT-2 (their queries staged in the last level's region)
-  for (int l = lv0; l < MT - 1; ++l) {
-    // level 6 of an 8-level tree reuses level 0's staging region: every warp's
-    // TMEM copy must be done
-    if (MT == 8 && l == MT - 2) __syncthreads();
-    if (active) {
-      load_cw(l + 1, cwn);                           // prefetch the next level's codeword
-      item(tab_s + ((uint32_t)(l - lv0) << 15), region_s + (uint32_t)l * kStageLevelBytes, cw);
-#pragma unroll
-      for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
-    }
-  }
-  __syncthreads();                                   // region free: build the last level into it
-  phase_mark(unit, 7);
-  if (active) item(region_s, stage_s, cw);
-  __syncthreads();
-  if constexpr (MT == 8) tmem_fence_after();         // TMEM level 0 visible to the scan's tcgen05.ld
-}
-
-// Few queries with long sub-vectors (c3: s = 60, <= 8 queries per CTA): one
-// staging pass per level (the small stage holds 8 queries x 64 dims), each
-// warp owns codeword block kb = w & 7 and the queries g, g+2, g+4, g+6
-// (g = w >> 3) and runs the whole j-ascending FMA chain of each entry in
-// registers over 16-dimension codeword chunks (next chunk prefetched) -- two
-// barriers per level instead of two per 16-dimension pass.
-template <int SS>
-__device__ void build_tables_wide(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq, int cell) {
-  static_assert(SS > kDC && SS <= 64 && SS % 4 == 0, "wide staging: 16 < s <= 64, s % 4 == 0");
-  constexpr int NCH = (SS + kDC - 1) / kDC;
-  const TreeDev& tr = p.tree[t];
-  const int MT = tr.MT;
-  const int lv0 = (MT == 8) ? 1 : 0;
-  const int K = p.K, d = p.d;
-  const int lane = lane_id(), warp = warp_id();
-  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
-  const int kb = warp & 7, g = warp >> 3;
-  const int k = kb * 32 + lane;
-  const bool kvalid = k < K;
-  const int si = threadIdx.x >> 6, sj = threadIdx.x & 63;   // staging element (8 x 64)
-  const int sq = (si < nq) ? sm.qidx[si] : -1;
-  auto fetch = [&](int l) -> float {
-    if (sq < 0 || sj >= SS) return 0.f;
-    const int m = p.lsub[tr.layer0 + l];
-    float v = __ldg(p.queries + (size_t)sq * d + (size_t)m * SS + sj);
-    if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * SS + sj);
-    return v;
-  };
-  float nxt = fetch(0);
-  __syncthreads();                              // previous users of the stage are done
-  sm.stage[threadIdx.x] = nxt;
-  __syncthreads();
-  for (int l = 0; l < MT; ++l) {
-    if (l + 1 < MT) nxt = fetch(l + 1);         // next level's stage value
-    const int m = p.lsub[tr.layer0 + l];
-    const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    float c[kDC], cn[kDC];
-#pragma unroll
-    for (int j = 0; j < kDC; j += 4) {
-      const float4 v = (j < SS) ? __ldg(reinterpret_cast<const float4*>(crow + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
-    }
-#pragma unroll
-    for (int jc = 0; jc < NCH; ++jc) {
-      if (jc + 1 < NCH) {
-#pragma unroll
-        for (int j = 0; j < kDC; j += 4) {
-          const int jj = (jc + 1) * kDC + j;
-          const float4 v = (jj < SS) ? __ldg(reinterpret_cast<const float4*>(crow + jj)) : make_float4(0.f, 0.f, 0.f, 0.f);
-          cn[j] = v.x; cn[j + 1] = v.y; cn[j + 2] = v.z; cn[j + 3] = v.w;
-        }
-      }
-      constexpr int NJ0 = SS - (NCH - 1) * kDC;   // size of the last chunk
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const int i = g + 2 * qq;
-        if (i < nq) {
-          const float* x = sm.stage + i * 64 + jc * kDC;
-#pragma unroll
-          for (int j = 0; j < kDC; ++j) {
-            if (jc < NCH - 1 || j < NJ0) {
-              const float tt = x[j] - c[j];
-              acc[qq] = fmaf(tt, tt, acc[qq]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kDC; ++j) c[j] = cn[j];
-    }
-#pragma unroll
-    for (int qq = 0; qq < 4; ++qq) {
-      const int i = g + 2 * qq;
-      if (i < nq && kvalid) *tab_slot(sm, lut0, l, lv0, k, i) = acc[qq];
-    }
-    __syncthreads();
-    if (l + 1 < MT) sm.stage[threadIdx.x] = nxt;
-    __syncthreads();
-  }
-}
-
-// Build the tables of tree t for this CTA's queries (fused).
-// Passes over (level, 16-dimension chunk): the chunk of the active queries'
-// sub-vectors (minus the coarse centroid for IVF residuals) is staged in shared
-// memory -- the next pass's values are prefetched into registers while the
-// current pass computes -- and each warp computes 32 codewords (one per lane,
-// codeword chunk in registers) against a share of the queries.  Entries are
-// accumulated across chunks in place, so every entry is the j-ascending fp32
-// FMA chain sum_j (x_j - c_j)^2 regardless of the chunking.
-template <int SS, int DC = kDC>
-__device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq, int cell) {
-  const TreeDev& tr = p.tree[t];
-  const int MT = tr.MT;
-  const int lv0 = (MT == 8) ? 1 : 0;
-  const int K = p.K, d = p.d;
-  const int s = (SS > 0) ? SS : p.s;
-  const int nb = (K + 31) >> 5;
-  const int lane = lane_id(), warp = warp_id();
-  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
-  if (p.luts) {   // materialised tables: copy
-    for (int item = warp; item < MT * nb; item += kWarps) {
-      const int l = item / nb, kb = item - l * nb;
-      const int k = kb * 32 + lane;
-      const int m = p.lsub[tr.layer0 + l];
-      for (int i = 0; i < nq; ++i) {
-        const float v = (k < K) ? __ldg(p.luts + ((size_t)sm.qidx[i] * p.M + m) * K + k) : 0.f;
-        if (k < K) *tab_slot(sm, lut0, l, lv0, k, i) = v;
-      }
-    }
-    return;
-  }
-  const int npl = (s + DC - 1) / DC;            // passes per level
-  const int P = MT * npl;
-  const int G = max(1, kWarps / nb);            // query groups
-  const int kb = warp % nb, g = warp / nb;
-  const bool computes = g < G;
-  // staging element of this thread: query slot si, dimension sj of the chunk
-  const int si = threadIdx.x / DC, sj = threadIdx.x % DC;
-  const int sq = (si < nq) ? sm.qidx[si] : -1;
-  auto fetch = [&](int pass) -> float {
-    const int l = pass / npl, jc = pass - l * npl;
-    const int j = jc * DC + sj;
-    if (sq < 0 || j >= s) return 0.f;
-    const int m = p.lsub[tr.layer0 + l];
-    float v = __ldg(p.queries + (size_t)sq * d + (size_t)m * s + j);
-    if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * s + j);
-    return v;
-  };
-  // codeword chunk of pass `pass` for this lane's codeword (registers)
-  const int k = kb * 32 + lane;
-  const bool kvalid = computes && k < K;
-  auto fetch_cw = [&](int pass, float (&c)[DC]) {
-    const int l = pass / npl, jc = pass - l * npl;
-    const int j0 = jc * DC;
-    const int nj = min(DC, s - j0);
-    const int m = p.lsub[tr.layer0 + l];
-    const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * s + j0;
-    if (p.vec4 && (s & 3) == 0) {   // 16-byte aligned rows: float4 loads
-#pragma unroll
-      for (int j = 0; j < DC; j += 4) {
-        const float4 v = (j < nj) ? __ldg(reinterpret_cast<const float4*>(crow + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        c[j] = v.x; c[j + 1] = v.y; c[j + 2] = v.z; c[j + 3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < DC; ++j) c[j] = (j < nj) ? __ldg(crow + j) : 0.f;
-    }
-  };
-  // DC == kDC: the next pass's codeword chunk is prefetched into registers;
-  // wide passes (DC > kDC, few queries) load it at the pass start instead
-  constexpr bool kPrefetchCw = (DC == kDC);
-  float cw[DC], cwn[kPrefetchCw ? DC : 1];
-  fetch_cw(0, cw);
-  float nxt = fetch(0);
-  __syncthreads();                              // previous users of the stage are done
-  if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
-  __syncthreads();
-  for (int pass = 0; pass < P; ++pass) {
-    if (pass + 1 < P) {                         // prefetch the next pass: stage values (+ codeword chunk)
-      nxt = fetch(pass + 1);
-      if constexpr (kPrefetchCw) fetch_cw(pass + 1, cwn);
-    }
-    const int l = pass / npl, jc = pass - l * npl;
-    const int nj = min(DC, s - jc * DC);
-    if (computes) {
-      if constexpr (SS > 0 && SS % DC == 0) {
-        build_pass_fixed<DC, DC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
-      } else if constexpr (SS > 0) {
-        if (nj == DC) build_pass_fixed<DC, DC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
-        else build_pass_fixed<(SS % DC) ? (SS % DC) : DC, DC>(sm, lut0, l, lv0, k, kvalid, cw, nq, g, G, jc == 0);
-      } else {
-        build_pass_generic(sm, lut0, l, lv0, k, kvalid, cw, nj, nq, g, G, jc == 0);
-      }
-    }
-    __syncthreads();
-    if (pass + 1 < P) {
-      if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
-      if constexpr (kPrefetchCw) {
-#pragma unroll
-        for (int j = 0; j < DC; ++j) cw[j] = cwn[j];
-      } else {
-        fetch_cw(pass + 1, cw);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// Warp-cooperative pruning of one lane's candidate buffer (rare; see DESIGN.md
-// §4.3).  Keeps every candidate that can still be among the query's k smallest
-// (distance, id) pairs: t = smallest distance whose cumulative multiplicity
-// reaches k; all candidates < t; of the candidates == t, those whose smallest
-// id ranks below k - (multiplicity < t).  Returns the new count and threshold.
-constexpr int kRefreshPer = (2 * kTopkMax + 96) / 32;   // entries per lane held in registers
-
-__device__ __noinline__ void refresh_buffer(uint2* buf, int n, int k, const uint32_t* gmult,
-                                            const int32_t* gminid, int* new_cnt, float* new_thr) {
-  const int lane = lane_id();
-  uint32_t key[kRefreshPer], grp[kRefreshPer], mul[kRefreshPer];
-#pragma unroll
-  for (int r = 0; r < kRefreshPer; ++r) {
-    const int i = r * 32 + lane;
-    if (i < n) {
-      uint2 e = buf[i];
-      key[r] = e.x; grp[r] = e.y; mul[r] = __ldg(gmult + e.y);
-    } else {
-      key[r] = 0xffffffffu; grp[r] = 0; mul[r] = 0;
-    }
-  }
-  // total multiplicity
-  uint32_t tot = 0;
-#pragma unroll
-  for (int r = 0; r < kRefreshPer; ++r) tot += mul[r];
-  tot = __reduce_add_sync(FULLMASK, tot);
-  if (tot < (uint32_t)k) {  // cannot prune (only possible with a tiny k vs B; keep all)
-    *new_cnt = n; *new_thr = __int_as_float(0x7f800000); return;
-  }
-  uint32_t v = 0;
-  for (int bit = 31; bit >= 0; --bit) {
-    const uint32_t cand = v | ((1u << bit) - 1u);
-    uint32_t c = 0;
-#pragma unroll
-    for (int r = 0; r < kRefreshPer; ++r) c += (key[r] <= cand) ? mul[r] : 0u;
-    c = __reduce_add_sync(FULLMASK, c);
-    if (c < (uint32_t)k) v |= (1u << bit);
-  }
-  const uint32_t t = v;
-  uint32_t slt = 0, ntied = 0;
-#pragma unroll
-  for (int r = 0; r < kRefreshPer; ++r) {
-    slt += (key[r] < t) ? mul[r] : 0u;
-    ntied += (key[r] == t) ? 1u : 0u;
-  }
-  slt = __reduce_add_sync(FULLMASK, slt);
-  ntied = __reduce_add_sync(FULLMASK, ntied);
-  const uint32_t R = (uint32_t)k - slt;
-  uint32_t tau = 0xffffffffu;
-  uint32_t mid[kRefreshPer];
-#pragma unroll
-  for (int r = 0; r < kRefreshPer; ++r) mid[r] = 0xffffffffu;
-  if (ntied > R) {
-#pragma unroll
-    for (int r = 0; r < kRefreshPer; ++r)
-      if (key[r] == t) mid[r] = (uint32_t)__ldg(gminid + grp[r]);
-    uint32_t w = 0;
-    for (int bit = 31; bit >= 0; --bit) {
-      const uint32_t cand = w | ((1u << bit) - 1u);
-      uint32_t c = 0;
-#pragma unroll
-      for (int r = 0; r < kRefreshPer; ++r) c += (key[r] == t && mid[r] <= cand) ? 1u : 0u;
-      c = __reduce_add_sync(FULLMASK, c);
-      if (c < R) w |= (1u << bit);
-    }
-    tau = w;
-  }
-  __syncwarp();
-  int base = 0;
-  const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int r = 0; r < kRefreshPer; ++r) {
-    const bool keep = (r * 32 + lane < n) && (key[r] < t || (key[r] == t && (ntied <= R || mid[r] <= tau)));
-    const unsigned m = __ballot_sync(FULLMASK, keep);
-    if (keep) buf[base + __popc(m & lt)] = make_uint2(key[r], grp[r]);
-    base += __popc(m);
-  }
-  __syncwarp();
-  *new_cnt = base;
-  *new_thr = __uint_as_float(t);
-}
-
-// Per-lane top-k candidate state.
-struct TopkState {
-  float thr;
-  int cnt;
-  uint2* buf;         // this lane's buffer
-  uint2* warp_buf;    // lane 0's buffer of this warp (lane L's = warp_buf + L*kWarps*B)
-  bool active;
-};
-
-struct EmitCtx {
-  const ScanParams* p;
-  int role;           // 0: forest per-leaf partials (every tree), 1: single tree, leaves are the groups
-  int t;              // tree index for role 0
-  int unit, chunk;
-  int q;              // query of this lane (-1: idle lane)
-  float* part;        // this unit's partials base
-  TopkState ts;
-};
-
-// Append one group's distance to this lane's candidates if it can still be in
-// the top-k (hot path: no calls, no syncs).  Buffers are pruned at batch
-// boundaries by maybe_refresh, which keeps >= 64 free slots per lane (a batch
-// of 32 leaves of each of a warp's two streams).
-__device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, uint32_t mult) {
-  const ScanParams& p = *e.p;
-  if (p.mode == kModeFull) {
-    p.leafdist[((size_t)e.chunk * 32 + lane_id()) * p.n_groups + g] = dist;   // query-major rows
-    return;
-  }
-  TopkState& ts = e.ts;
-  if (ts.active && dist <= ts.thr) {
-    ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), g);
-    ++ts.cnt;
-    if (mult >= (uint32_t)p.k) ts.thr = dist;   // one group alone bounds the k-th distance
-  }
-}
-
-struct CntThr { int cnt; float thr; };
-
-// Per-query thresholds shared by every unit (CTA) that scans the query --
-// leaf segments, IVF probes -- through global atomicMin on the float bits
-// (distances are >= 0, so the bit order is the value order).  Initialised to
-// 0x7f7f7f7f (~3.4e38) by a memset; kThrNone marks "no bound yet".
-constexpr float kThrNone = 1e38f;
-
-__device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr, int B, int k,
-                                             const uint32_t* gmult, const int32_t* gminid) {
-  const int lane = lane_id();
-  // full buffers, and (once) buffers that first reach k candidates while the
-  // lane has no threshold yet: an early exact bound stops the flood of
-  // candidates that every fresh warp would otherwise emit
-  unsigned full = __ballot_sync(FULLMASK, cnt > B - 64 || (cnt >= k && !(thr < kThrNone)));
-  while (full) {
-    const int L = __ffs(full) - 1;
-    full &= full - 1;
-    int nc; float nt;
-    const int n = __shfl_sync(FULLMASK, cnt, L);
-    refresh_buffer(warp_buf + (size_t)L * kWarps * B, n, k, gmult, gminid, &nc, &nt);
-    if (lane == L) { cnt = nc; thr = fminf(thr, nt); }
-  }
-  return CntThr{cnt, thr};
-}
-
-__device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
-  const ScanParams& p = *e.p;
-  if (__any_sync(FULLMASK, e.ts.cnt > p.B - 64 || (e.ts.cnt >= p.k && !(e.ts.thr < kThrNone)))) {
-    const CntThr r = maybe_refresh(e.ts.warp_buf, e.ts.cnt, e.ts.thr, p.B, p.k, p.group_mult, p.group_minid);
-    e.ts.cnt = r.cnt;
-    e.ts.thr = r.thr;
-  }
-}
-
-// Leaf record: one uint4 = 8 half-words; half-word l is the
-// pre-swizzled byte offset of table entry (level l, k = code byte l) inside
-// that level's 32 KB shared-memory region, (k << 7) | ((k & 31) << 2), so a
-// lookup is one extract/XOR with the lane's offset and one LDS whose immediate
-// carries the level's region base.  Level 0 of an 8-level tree lives in TMEM:
-// its half-word is the column k (bits 0..7) with the LCP with the previous
-// leaf in bits 8..11 and floor(log2(multiplicity)) in bits 12..15; trees with
-// MT < 8 keep both in half-word 7 (bits 0..3, 4..7).
-#ifndef ET_SCAN_VARIANT
-#define ET_SCAN_VARIANT 3
-#endif
-
-// The scan kernel has no static shared memory, so its dynamic shared memory
-// (the tables, at offset 0) starts at the fixed shared-window address
-// kDsmBase (after the 1 KB the system reserves); scan_kernel traps if not.
-constexpr uint32_t kDsmBase = 0x400;
-
-
-template <int MT>
-__device__ __forceinline__ uint32_t rec_lcp(const uint4& r) {
-  if constexpr (MT == 8) return (r.x >> 8) & 15u;
-  else return (r.w >> 16) & 15u;
-}
-// floor(log2(multiplicity)) of the leaf's group (single trees), capped at 15:
-// 2^bucket >= k proves the group alone holds k ids (a conservative test)
-template <int MT>
-__device__ __forceinline__ uint32_t rec_mbucket(const uint4& r) {
-  if constexpr (MT == 8) return (r.x >> 12) & 15u;
-  else return (r.w >> 20) & 15u;
-}
-
-// Distance-Context update of one leaf, branch-free.  v[l] holds the table
-// entry T[l][k_l] of the path's node at depth l.  A leaf whose LCP with its
-// predecessor is p shares the nodes at depths < p, whose entries are still in
-// v[0..p-1]; it looks up levels p..MT-1 only (predicated LDS: the internal
-// nodes entered at depths p..depth-1, its own K, and its
-// postfix).  The distance is then the left-to-right sum
-// ((v0 + v1) + v2) + ... -- the Distance Context ctx[l] = ctx[l-1] + T[l][k_l]
-// of P:238-252 recomputed in registers, bit-identical to naive ADC.
-// `valid` = false makes the call a no-op on v (the padding leaf of a stream).
-template <int MT>
-__device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t pl, bool valid,
-                                         uint32_t lane4, uint32_t tq) {
-  constexpr int lv0 = (MT == 8) ? 1 : 0;
-  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-  const uint32_t plv = valid ? pl : 255u;   // 255: no level is looked up
-  if constexpr (lv0 == 1) {
-    // level 0 (TMEM) only on a new first-level subtree: a warp-uniform predicate
-    uint32_t t0 = __float_as_uint(v[0]);
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.u32 q, %2, 0;\n\t"
-                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
-                 : "+r"(t0) : "r"(tq + (w[0] & 255u)), "r"(plv));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0));
-    v[0] = __uint_as_float(t0);
-  }
-#pragma unroll
-  for (int l = lv0; l < MT; ++l) {
-    const uint32_t off = (l & 1) ? ((w[l >> 1] >> 16) ^ lane4) : ((w[l >> 1] & 0xffffu) ^ lane4);
-    const uint32_t addr = off + (kDsmBase + ((uint32_t)(l - lv0) << 15));
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.le.u32 q, %2, %3;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
-                 : "+f"(v[l]) : "r"(addr), "r"(plv), "r"((uint32_t)l));
-  }
-  float s = v[0];
-#pragma unroll
-  for (int l = 1; l < MT; ++l) s = s + v[l];
-  return s;
-}
-
-// Scan of leaves [a, b) of one tree by one warp, lane = query.  The range is
-// split into two halves scanned in lockstep (two independent dependency
-// chains per warp); records come with one coalesced load per 32 leaves per
-// half (the next batch in flight) and four shuffles per leaf.  A leaf costs
-// (MT - LCP) shared-memory lookups, MT - 1 FADDs and no branches.
-template <int MT, int ROLE>
-__device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b,
-                          const float* lut0g) {
-  (void)lut0g;
-  const ScanParams& p = *e.p;
-  const int lane = lane_id();
-  const uint32_t lane4 = (uint32_t)lane << 2;
-  const uint32_t tq = tmem_lane_base(sm.tmem);
-  const bool topk = p.mode == kModeTopk;
-  const uint4* rec = tr.rec;
-  auto shfl_rec = [&](const uint4& mine, int j) {
-    uint4 r;
-    r.x = __shfl_sync(FULLMASK, mine.x, j);
-    r.y = (MT > 2) ? __shfl_sync(FULLMASK, mine.y, j) : 0u;
-    r.z = (MT > 4) ? __shfl_sync(FULLMASK, mine.z, j) : 0u;
-    r.w = __shfl_sync(FULLMASK, mine.w, j);   // levels 6-7, or the LCP when MT < 8
-    return r;
-  };
-  auto load_batch = [&](uint32_t base, uint32_t end) {
-    return (base + lane < end) ? __ldg(rec + base + lane) : make_uint4(0u, 0u, 0u, 0u);
-  };
-  auto batch_end = [&]() {
-    if (topk && ROLE != 0) {   // prune full buffers; share the threshold with the CTA's other warps
-      refresh_if_needed(e);    // and with every other unit scanning the same query
-      if (e.ts.active) {
-        const unsigned mine = __float_as_uint(e.ts.thr);
-        atomicMin(&sm.thr[lane], mine);
-        unsigned t = *((volatile unsigned*)&sm.thr[lane]);
-        if (p.qthr_shared) t = min(t, atomicMin(p.qthr + e.q, t));
-        e.ts.thr = __uint_as_float(t);
-      }
-    }
-  };
-  {
-    const uint32_t m = a + (b - a + 1) / 2;   // halves [a, m) and [m, b); |[m, b)| <= |[a, m)|
-    float v0[MT], v1[MT];
-#pragma unroll
-    for (int l = 0; l < MT; ++l) { v0[l] = 0.f; v1[l] = 0.f; }
-    uint4 nx0 = load_batch(a, m), nx1 = load_batch(m, b);
-    auto emit = [&](uint32_t leaf, float dist, const uint4& r, bool valid) {
-      if constexpr (ROLE == 0) {
-        if (valid) e.part[(size_t)p.part_base[e.t] + (size_t)leaf * 32 + lane] = dist;
-      } else {
-        if (p.mode == kModeFull) {
-          if (valid) p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + leaf] = dist;   // query-major rows
-        } else {
-          TopkState& ts = e.ts;
-          const bool em = valid && ts.active && dist <= ts.thr;
-          if (em) ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), leaf);
-          ts.cnt += em ? 1 : 0;
-          // one group alone (2^bucket <= multiplicity ids) bounds the k-th distance
-          if (em && (1u << rec_mbucket<MT>(r)) >= (uint32_t)p.k) ts.thr = dist;
-        }
-      }
-    };
-    for (uint32_t off = 0; a + off < m; off += 32) {
-      const uint4 mine0 = nx0, mine1 = nx1;
-      nx0 = load_batch(a + off + 32, m);
-      nx1 = load_batch(m + off + 32, b);
-      const int n0 = (int)min(32u, m - (a + off));
-      const int n1 = (m + off < b) ? (int)min(32u, b - (m + off)) : 0;
-      for (int j = 0; j < n0; ++j) {
-        const uint4 r0 = shfl_rec(mine0, j), r1 = shfl_rec(mine1, j);
-        const uint32_t leaf0 = a + off + j, leaf1 = m + off + j;
-        const bool ok1 = j < n1;
-        const uint32_t pl0 = (off + j == 0) ? 0u : rec_lcp<MT>(r0);   // range starts: rebuild the path
-        const uint32_t pl1 = (off + j == 0) ? 0u : rec_lcp<MT>(r1);
-        const float d0 = dc_leaf<MT>(v0, r0, pl0, true, lane4, tq);
-        const float d1 = dc_leaf<MT>(v1, r1, pl1, ok1, lane4, tq);
-        emit(leaf0, d0, r0, true);
-        emit(leaf1, d1, r1, ok1);
-      }
-      batch_end();
-    }
-  }
-}
-
-// Prune full candidate buffers and share the lanes' thresholds with the CTA's
-// other warps (shared memory) and, when a query spans several units, with
-// every unit scanning it (global per-query atomicMin).
-__device__ __forceinline__ void share_threshold(EmitCtx& e, const SmemScan& sm) {
-  const ScanParams& p = *e.p;
-  const int lane = lane_id();
-  refresh_if_needed(e);
-  if (e.ts.active) {
-    atomicMin(&sm.thr[lane], __float_as_uint(e.ts.thr));
-    unsigned t = *((volatile unsigned*)&sm.thr[lane]);
-    if (p.qthr_shared) t = min(t, atomicMin(p.qthr + e.q, t));
-    e.ts.thr = __uint_as_float(t);
-  }
-}
-
-// E-Forest join (reading A13): every tuple -- one distinct full
-// code, i.e. one group -- gets dist = ((p_0 + p_1) + ...) summed in tree order
-// from the per-tree partials of its leaves (written by the trees' scans).
-// Tuples [ga, gb) of this warp, 32 at a time: their leaves and multiplicities
-// in one coalesced load each, then the per-query partials (coalesced across
-// lanes) kJoinBatch tuples at a time.
-constexpr int kJoinBatch = 16;   // tuples whose partials are in flight at once
-
-__device__ void join_tuples(EmitCtx& e, const SmemScan& sm, uint32_t ga, uint32_t gb) {
-  const ScanParams& p = *e.p;
-  const int lane = lane_id();
-  const bool topk = p.mode == kModeTopk;
-  for (uint32_t g0 = ga; g0 < gb; g0 += 32) {
-    const int n = (int)min(32u, gb - g0);
-    uint32_t my_l[kMaxTrees];
-#pragma unroll
-    for (int t = 0; t < kMaxTrees; ++t) my_l[t] = (t < p.T && lane < n) ? __ldg(p.tup_leaf[t] + g0 + lane) : 0u;
-    const uint32_t my_mu = (topk && lane < n) ? __ldg(p.group_mult + g0 + lane) : 0u;
-    for (int u0 = 0; u0 < n; u0 += kJoinBatch) {
-      float acc[kJoinBatch];
-#pragma unroll
-      for (int u = 0; u < kJoinBatch; ++u) {
-        const uint32_t l0 = __shfl_sync(FULLMASK, my_l[0], u0 + u);
-        acc[u] = (u0 + u < n) ? e.part[(size_t)p.part_base[0] + (size_t)l0 * 32 + lane] : 0.f;
-      }
-#pragma unroll
-      for (int t = 1; t < kMaxTrees; ++t) {
-        if (t < p.T) {
-          float pv[kJoinBatch];
-#pragma unroll
-          for (int u = 0; u < kJoinBatch; ++u) {
-            const uint32_t lt = __shfl_sync(FULLMASK, my_l[t], u0 + u);
-            pv[u] = (u0 + u < n) ? e.part[(size_t)p.part_base[t] + (size_t)lt * 32 + lane] : 0.f;
-          }
-#pragma unroll
-          for (int u = 0; u < kJoinBatch; ++u) acc[u] = acc[u] + pv[u];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kJoinBatch; ++u) {
-        const uint32_t mult = __shfl_sync(FULLMASK, my_mu, u0 + u);
-        if (u0 + u < n) emit_group(e, acc[u], g0 + u0 + u, mult);
-      }
-    }
-    if (topk) share_threshold(e, sm);
-  }
-}
-
-template <int ROLE>
-__device__ __forceinline__ void scan_dispatch(EmitCtx& e, const SmemScan& sm, const TreeDev& tr,
-                                              uint32_t a, uint32_t b, const float* lut0g) {
-  switch (tr.MT) {
-    case 1: scan_tree<1, ROLE>(e, sm, tr, a, b, lut0g); break;
-    case 2: scan_tree<2, ROLE>(e, sm, tr, a, b, lut0g); break;
-    case 3: scan_tree<3, ROLE>(e, sm, tr, a, b, lut0g); break;
-    case 4: scan_tree<4, ROLE>(e, sm, tr, a, b, lut0g); break;
-    case 5: scan_tree<5, ROLE>(e, sm, tr, a, b, lut0g); break;
-    case 6: scan_tree<6, ROLE>(e, sm, tr, a, b, lut0g); break;
-    case 7: scan_tree<7, ROLE>(e, sm, tr, a, b, lut0g); break;
-    case 8: scan_tree<8, ROLE>(e, sm, tr, a, b, lut0g); break;
-    default: break;
-  }
-}
-
-// MTC > 0: every tree has MTC levels (compile time); 0: runtime switch.
-template <int MTC, int ROLE>
-__device__ __forceinline__ void scan_any(EmitCtx& e, const SmemScan& sm, const TreeDev& tr,
-                                         uint32_t a, uint32_t b, const float* lut0g) {
-  if constexpr (MTC > 0) scan_tree<MTC, ROLE>(e, sm, tr, a, b, lut0g);
-  else scan_dispatch<ROLE>(e, sm, tr, a, b, lut0g);
-}
-
-struct FinWarp;
-__device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q);
-__device__ void finalize_fused(const FinParams& p, unsigned char* smem, const int* qidx, int nq);
-
-template <int SS, int MTC, bool FOREST>
-__global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant__ ScanParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int unit = blockIdx.x;
-  const int chunk = unit / p.S;
-  const int seg = unit - chunk * p.S;
-  const int lane = lane_id(), warp = warp_id();
-  if (threadIdx.x == 0 && smem_u32(smem_raw) != kDsmBase) __trap();   // tab_ld's fixed base
-  phase_mark(unit, 0);
-  if (p.n_chunks_dev && chunk >= *p.n_chunks_dev) return;   // IVF: fewer chunks than the bound
-  int MTmax = 0;
-  for (int t = 0; t < p.T; ++t) MTmax = max(MTmax, p.tree[t].MT);
-  const int smem_levels = (MTmax == 8) ? 7 : MTmax;
-  // resident build of the first tree: stage the queries asynchronously now
-  constexpr bool kResident = (SS == kDC && MTC > 0);
-  const bool staged = kResident && !p.luts && !p.chunk_cell;
-  if constexpr (kResident) {
-    if (staged) {
-      const int MTf = p.tree[p.T - 1].MT;
-      const size_t reg = ((size_t)smem_levels * 256 * 32 * 4 > (size_t)kFinRegion) ? (size_t)smem_levels * 256 * 32 * 4
-                                                                                    : (size_t)kFinRegion;
-      const uint32_t base = smem_u32(smem_raw);
-      const uint32_t region_s = base + ((uint32_t)(MTf - 1 - (MTf == 8 ? 1 : 0)) << 15);
-      const uint32_t stage_s = base + (uint32_t)reg + 32u * 4u + 32u * 4u;   // = sm.stage below
-      stage_async<SS, MTC>(p, p.T - 1, chunk, p.n_units / p.S, region_s, stage_s);
-    }
-  }
-  SmemScan sm;
-  sm.tab = reinterpret_cast<float*>(smem_raw);
-  const size_t region = ((size_t)smem_levels * 256 * 32 * 4 > (size_t)kFinRegion) ? (size_t)smem_levels * 256 * 32 * 4
-                                                                                    : (size_t)kFinRegion;
-  sm.thr = reinterpret_cast<unsigned*>(smem_raw + region);
-  sm.qidx = reinterpret_cast<int*>(sm.thr + 32);
-  sm.stage = reinterpret_cast<float*>(sm.qidx + 32);
-  sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.stage + 32 * kDC);
-  sm.tmem = 0;
-  const bool use_tmem = (MTmax == 8);
-  if (use_tmem) {
-    if (warp == 0) tmem_alloc(sm.tmem_slot);
-    tmem_fence_before();
-  }
-
-  if (threadIdx.x < 32) {
-    if (p.flatQ > 0) {
-      const int nch = p.n_units / p.S;
-      const int64_t s0 = (int64_t)chunk * p.flatQ / nch, s1 = (int64_t)(chunk + 1) * p.flatQ / nch;
-      sm.qidx[lane] = (s0 + lane < s1) ? (int)(s0 + lane) : -1;
-    } else {
-      sm.qidx[lane] = __ldg(p.chunk_q + (size_t)chunk * 32 + lane);
-    }
-    sm.thr[lane] = 0x7f800000u;   // +inf
-  }
-  __syncthreads();
-  if (use_tmem) {
-    tmem_fence_after();
-    sm.tmem = *sm.tmem_slot;
-  }
-  int nq = 0;
-  {
-    const int q = sm.qidx[lane];
-    nq = __popc(__ballot_sync(FULLMASK, q >= 0));   // active lanes are a prefix
-  }
-  const int cell = p.chunk_cell ? __ldg(p.chunk_cell + chunk) : -1;
-  const float* lut0g = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
-
-  EmitCtx e;
-  e.p = &p;
-  e.unit = unit;
-  e.chunk = chunk;
-  e.q = sm.qidx[lane];
-  e.part = p.partials ? p.partials + (size_t)unit * p.part_stride : nullptr;
-  e.ts.active = lane < nq;
-  e.ts.thr = e.ts.active ? __int_as_float(0x7f800000) : -1.0f;
-  e.ts.cnt = 0;
-  e.ts.warp_buf = nullptr;
-  e.ts.buf = nullptr;
-  if (p.mode == kModeTopk) {
-    // candidates of (unit, lane): kWarps consecutive per-warp buffers of B entries
-    e.ts.warp_buf = p.cand + ((size_t)unit * 32 * kWarps + warp) * p.B;
-    e.ts.buf = e.ts.warp_buf + (size_t)lane * kWarps * p.B;
-  }
-
-  // Forest: trees T-1..1 first (per-leaf partials for this CTA's queries),
-  // then tree 0, whose leaves walk their tuples and sum in tree order.
-  for (int t = p.T - 1; t >= 0; --t) {
-    const TreeDev& tr = p.tree[t];
-    bool level0_done = false;   // resident build copies level 0 to TMEM itself
-    if constexpr (SS == kDC && MTC > 0) {
-      if (p.luts) { build_tables<SS>(p, sm, t, unit, nq, cell); __syncthreads(); }
-      else {
-        phase_mark(unit, 1);
-        build_tables_resident<SS, MTC>(p, sm, t, unit, nq, cell, staged && t == p.T - 1);
-        level0_done = true;
-        phase_mark(unit, 2);
-      }
-    } else {
-      if constexpr (SS > kDC && SS <= 64 && SS % 4 == 0) {
-        if (nq <= 8 && !p.luts && p.vec4) build_tables_wide<SS>(p, sm, t, unit, nq, cell);
-        else build_tables<SS>(p, sm, t, unit, nq, cell);
-      } else {
-        build_tables<SS>(p, sm, t, unit, nq, cell);
-      }
-      __syncthreads();
-    }
-    if (tr.MT == 8 && !level0_done) {   // level 0 -> TMEM (every warp copies a quarter of its quadrant's columns)
-      tmem_fence_after();
-      tmem_load_level0(sm, lut0g);
-      tmem_fence_before();
-      __syncthreads();
-      tmem_fence_after();
-    }
-    uint32_t lo = 0, hi = (uint32_t)tr.n_leaves;
-    if (t == 0) {
-      if (p.chunk_lo) { lo = __ldg(p.chunk_lo + chunk); hi = __ldg(p.chunk_hi + chunk); }
-      const uint32_t len = hi - lo;
-      const uint32_t a = lo + (uint32_t)(((uint64_t)len * seg) / p.S);
-      const uint32_t b = lo + (uint32_t)(((uint64_t)len * (seg + 1)) / p.S);
-      lo = a; hi = b;
-    }
-    const uint32_t len = hi - lo;
-    const uint32_t wa = lo + (uint32_t)(((uint64_t)len * warp) / kWarps);
-    const uint32_t wb = lo + (uint32_t)(((uint64_t)len * (warp + 1)) / kWarps);
-    e.t = t;
-    if (wa < wb) {
-      if constexpr (FOREST) {
-        scan_any<MTC, 0>(e, sm, tr, wa, wb, lut0g);   // per-leaf partials of every tree
-      } else {
-        scan_any<MTC, 1>(e, sm, tr, wa, wb, lut0g);
-      }
-    }
-    tmem_fence_before();
-    __syncthreads();   // partials visible / tables free for the next tree
-    tmem_fence_after();
-  }
-  if constexpr (FOREST) {   // the CTA's warps split the tuples evenly
-    const uint64_t G = (uint64_t)p.n_groups;
-    join_tuples(e, sm, (uint32_t)((G * warp) / kWarps), (uint32_t)((G * (warp + 1)) / kWarps));
-  }
-  phase_mark(unit, 3);
-  if (use_tmem && warp == 0) tmem_dealloc(sm.tmem);
-
-  if (p.mode == kModeTopk && p.qthr && !p.qthr_shared && warp == 0 && sm.qidx[lane] >= 0)
-    p.qthr[sm.qidx[lane]] = sm.thr[lane];   // the query's only unit: its final threshold
-  if (p.mode == kModeTopk && !p.compact) {
-    // per-warp candidate lists stay where the scan wrote them: lane L's 16
-    // buffers are contiguous, counts at cand_cnt[(unit*32 + L)*kWarps + warp]
-    p.cand_cnt[((size_t)unit * 32 + lane) * kWarps + warp] = e.ts.cnt;
-    if (warp == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + lane] = __uint_as_float(sm.thr[lane]);
-  } else if (p.mode == kModeTopk) {
-    // Long lists (small groups): merge the 16 warps' candidates of each lane
-    // into its first buffer under the final threshold, in place -- lane L's
-    // buffers are contiguous, so write position <= read position.
-    int* cnt_s = reinterpret_cast<int*>(smem_raw);   // tables are dead now
-    cnt_s[warp * 32 + lane] = e.ts.cnt;
-    __syncthreads();
-    for (int L = warp; L < 32; L += kWarps) {
-      const int myc = (lane < kWarps) ? cnt_s[lane * 32 + L] : 0;
-      int inc = myc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULLMASK, inc, o);
-        if (lane >= o) inc += y;
-      }
-      const int total = __shfl_sync(FULLMASK, inc, 31);
-      const int excl = inc - myc;
-      uint32_t tb = sm.thr[L];
-      if (p.qthr && sm.qidx[L] >= 0) tb = min(tb, *((volatile unsigned*)(p.qthr + sm.qidx[L])));
-      uint2* base = p.cand + ((size_t)unit * 32 + L) * kWarps * p.B;
-      int n = 0;
-      for (int i0 = 0; i0 < total; i0 += 32) {
-        const int idx = i0 + lane;
-        int w = 0;
-#pragma unroll
-        for (int st = 8; st >= 1; st >>= 1) {
-          const int o = __shfl_sync(FULLMASK, excl, (w + st) & 31);
-          if (w + st < kWarps && o <= idx) w += st;
-        }
-        const int wo = __shfl_sync(FULLMASK, excl, w & 31);
-        uint2 v = make_uint2(0xffffffffu, 0);
-        if (idx < total) v = base[(size_t)w * p.B + (idx - wo)];
-        const bool keep = (idx < total) && v.x <= tb;
-        const unsigned m = __ballot_sync(FULLMASK, keep);
-        __syncwarp();
-        if (keep) base[n + __popc(m & ((1u << lane) - 1u))] = v;
-        n += __popc(m);
-      }
-      // exact unit-level top-k of the merged list (it fits the warp's registers):
-      // at most ~k survivors per unit and a tight per-query bound for the
-      // other units and the finalize prefilter
-      constexpr int kCap = kRefreshPer * 32;
-      bool tightened = false;
-      while (n > kCap) {
-        // longer lists: the exact k-th of the first kCap entries bounds the
-        // query's k-th distance; filter the rest by it (in place) and repeat
-        __syncwarp();
-        int nc;
-        float nt;
-        refresh_buffer(base, kCap, p.k, p.group_mult, p.group_minid, &nc, &nt);
-        const uint32_t ntb = __float_as_uint(nt);
-        int m = nc;
-        for (int i0 = kCap; i0 < n; i0 += 32) {
-          const int idx = i0 + lane;
-          uint2 v = make_uint2(0xffffffffu, 0);
-          if (idx < n) v = base[idx];
-          const bool keep = (idx < n) && v.x <= ntb;
-          const unsigned mk = __ballot_sync(FULLMASK, keep);
-          __syncwarp();
-          if (keep) base[m + __popc(mk & ((1u << lane) - 1u))] = v;
-          m += __popc(mk);
-        }
-        __syncwarp();
-        tb = min(tb, ntb);
-        tightened = true;
-        if (m >= n) break;   // no progress (ties): leave the list as it is
-        n = m;
-      }
-      if (n > p.k && n <= kCap) {
-        __syncwarp();
-        int nc;
-        float nt;
-        refresh_buffer(base, n, p.k, p.group_mult, p.group_minid, &nc, &nt);
-        n = nc;
-        tb = min(tb, __float_as_uint(nt));
-        tightened = true;
-      }
-      if (tightened && p.qthr && lane == 0 && sm.qidx[L] >= 0) atomicMin(p.qthr + sm.qidx[L], tb);
-      if (lane < kWarps) p.cand_cnt[((size_t)unit * 32 + L) * kWarps + lane] = (lane == 0) ? n : 0;
-      if (lane == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + L] = __uint_as_float(tb);
-    }
-  }
-  if (p.mode == kModeTopk && p.fuse_fin) {   // every query of this chunk was scanned by this CTA alone
-    __threadfence_block();
-    __syncthreads();
-    finalize_fused(p.fin, smem_raw, sm.qidx, nq);
-  }
-  phase_mark(unit, 4);
-}
-
-size_t scan_smem_bytes(int MTmax) {
-  const int levels = (MTmax == 8) ? 7 : MTmax;
-  const size_t tab = (size_t)levels * 256 * 32 * 4;
-  return (tab > (size_t)kFinRegion ? tab : (size_t)kFinRegion) + 32 * 4 + 32 * 4 + 32 * kDC * 4 + 16;
-}
-
-template <int SS, int MTC, bool FOREST>
-static cudaError_t launch_scan_t(const ScanParams& p, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS, MTC, FOREST>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  scan_kernel<SS, MTC, FOREST><<<p.n_units, kThreads, smem, st>>>(p);
-  count_launch();
-  return cudaGetLastError();
-}
-
-template <int SS>
-static cudaError_t launch_scan_s(const ScanParams& p, size_t smem, cudaStream_t st) {
-  bool uni = true;
-  for (int t = 1; t < p.T; ++t) uni = uni && (p.tree[t].MT == p.tree[0].MT);
-  const int mt = uni ? p.tree[0].MT : 0;
-  const bool forest = p.T > 1;
-  if (mt == 8) return forest ? launch_scan_t<SS, 8, true>(p, smem, st) : launch_scan_t<SS, 8, false>(p, smem, st);
-  if (mt == 4) return forest ? launch_scan_t<SS, 4, true>(p, smem, st) : launch_scan_t<SS, 4, false>(p, smem, st);
-  return forest ? launch_scan_t<SS, 0, true>(p, smem, st) : launch_scan_t<SS, 0, false>(p, smem, st);
-}
-
+// K2 dispatch by sub-vector length (template instantiations live in scan_s*.cu)
 cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st) {
   if (p.n_units <= 0) return cudaSuccess;
-  const size_t smem = scan_smem_bytes(MTmax);
+  const int levels = (MTmax == 8) ? 7 : MTmax;
+  const size_t smem = (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + 32 * 16 * 4 + 16;   // = scan_smem_bytes
   const bool v4 = (p.luts == nullptr) && (p.d % 4 == 0) && p.vec4;
   switch (v4 ? p.s : 0) {
-    case 16: return launch_scan_s<16>(p, smem, st);
-    case 60: return launch_scan_s<60>(p, smem, st);
-    default: return launch_scan_s<0>(p, smem, st);
+    case 16: return launch_scan_16(p, smem, st);
+    case 60: return launch_scan_60(p, smem, st);
+    default: return launch_scan_0(p, smem, st);
   }
 }
+
 
 // ---------------------------------------------------------------------------
 // warp bitonic sort of n (power of two, <= 512) u64 keys in shared memory
@@ -1821,7 +460,6 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
   }
 }
 
-static_assert(sizeof(FinWarp) == kFinWarpBytes, "FinWarp layout");
 
 __global__ void __launch_bounds__(kFinWarps * 32) finalize_kernel(const __grid_constant__ FinParams p) {
   extern __shared__ __align__(16) unsigned char fsm_raw[];
@@ -1897,8 +535,8 @@ __device__ __forceinline__ void bitonic32(unsigned long long& a) {
   }
 }
 
-// One query, one warp.  own_fw: this warp's private slow-path scratch (the
-// scan kernel's fused finalize) or null (the standalone kernel's locked one).
+// One query, one warp.  own_fw: a private slow-path scratch, or null (the
+// CTA's shared one, taken under a lock).
 __device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t q, FinWarp* own_fw) {
   const int lane = lane_id();
   const int k = p.k;
@@ -2061,15 +699,6 @@ __global__ void __launch_bounds__(kFastWarps * 32, 6) finalize_fast_kernel(const
   const int64_t q = (int64_t)blockIdx.x * kFastWarps + warp_id();
   if (q >= p.Q) return;
   finalize_fast_query(p, q, nullptr);
-}
-
-// Fused finalize (scan kernel, every query of the CTA scanned by it alone).
-__device__ void finalize_fused(const FinParams& p, unsigned char* smem, const int* qidx, int nq) {
-  FinWarp* fw = reinterpret_cast<FinWarp*>(smem + (size_t)warp_id() * sizeof(FinWarp));
-  for (int i = warp_id(); i < nq; i += kWarps) {
-    if (p.fast) finalize_fast_query(p, qidx[i], fw);
-    else finalize_query(p, *fw, qidx[i]);
-  }
 }
 
 cudaError_t launch_finalize(const FinParams& p, cudaStream_t st) {
@@ -2400,7 +1029,7 @@ __global__ void __launch_bounds__(256) probe_kernel(const float* __restrict__ cT
       }
     }
 #pragma unroll
-    for (int qq = 0; qq < QB; ++qq) ds[qq * nlist + c] = acc[qq];
+    for (int qq = 0; qq < QB; ++qq) ds[qq * nlist + c] = (acc[qq] != acc[qq]) ? __int_as_float(0x7f800000) : acc[qq];   // NaN -> +inf
   }
   __syncthreads();
   const int lane = lane_id(), warp = warp_id();
@@ -2411,6 +1040,7 @@ __global__ void __launch_bounds__(256) probe_kernel(const float* __restrict__ cT
       int bc = INT_MAX;
       for (int c = lane; c < nlist; c += 32) {
         const float v = row[c];
+        if (v != v) continue;   // NaN marks a cell already taken (distances are never NaN: see above)
         if (v < bd || (v == bd && c < bc)) { bd = v; bc = c; }
       }
       for (int o = 16; o > 0; o >>= 1) {
@@ -2418,9 +1048,9 @@ __global__ void __launch_bounds__(256) probe_kernel(const float* __restrict__ cT
         const int oc = __shfl_xor_sync(FULLMASK, bc, o);
         if (od < bd || (od == bd && oc < bc)) { bd = od; bc = oc; }
       }
-      if (lane == 0) {
-        probes[(size_t)(q0 + qq) * w + r] = bc;
-        row[bc] = __int_as_float(0x7fc00000);   // NaN: never selected again
+      if (lane == 0) {   // w <= nlist, so a cell is always left (bc < nlist); guard anyway
+        probes[(size_t)(q0 + qq) * w + r] = (bc < nlist) ? bc : 0;
+        if (bc < nlist) row[bc] = __int_as_float(0x7fc00000);   // NaN: never selected again
       }
       __syncwarp();
     }
@@ -2523,10 +1153,3 @@ cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist
 }
 
 }  // namespace et
-
-#ifdef ET_PHASE_TIMING
-extern "C" int et_debug_phases(unsigned long long* out, int n_units) {
-  if (n_units > (1 << 16)) n_units = 1 << 16;
-  return (int)cudaMemcpyFromSymbol(out, et::g_phase, (size_t)n_units * 8 * sizeof(unsigned long long));
-}
-#endif

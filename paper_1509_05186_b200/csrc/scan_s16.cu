@@ -1,0 +1,14 @@
+// scan_s16.cu -- scan kernel instantiations for sub-vector length s = 16
+// (one translation unit per s so the kernel variants compile in parallel).
+#include "scan.cuh"
+
+namespace et {
+cudaError_t launch_scan_16(const ScanParams& p, size_t smem, cudaStream_t st) { return launch_scan_s<16>(p, smem, st); }
+}  // namespace et
+
+#ifdef ET_PHASE_TIMING
+extern "C" int et_debug_phases(unsigned long long* out, int n_units) {
+  if (n_units > (1 << 16)) n_units = 1 << 16;
+  return (int)cudaMemcpyFromSymbol(out, et::g_phase, (size_t)n_units * 8 * sizeof(unsigned long long));
+}
+#endif
