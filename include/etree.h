@@ -210,6 +210,25 @@ et_status et_merge_topk(const float* in_dist, const int32_t* in_ids, int32_t G,
                         int64_t Q, int32_t k, float* out_dist, int32_t* out_ids,
                         void* stream);
 
+/* Multi-GPU shard plan (host only, no GPU).  P:217-218: sub-structures built
+ * separately and concatenated form the whole HMS, so cutting the sorted codes
+ * between first-level subtrees (first code byte) gives G independent trees
+ * whose union of top-k lists is the global top-k.
+ * codes: HOST [n][M]; bounds: HOST int32 [G+1] output, bounds[0] = 0,
+ * bounds[G] = K; shard r holds the codes whose byte 0 is in
+ * [bounds[r], bounds[r+1]); bounds[r] (0 < r < G) is the smallest byte value
+ * v with G * #(byte0 < v) >= r * n (kept >= bounds[r-1]).  A shard may be
+ * empty (the caller then contributes (+inf, -1) lists).
+ * Errors: ET_ERR_CONFIG (null pointer, G < 1, K outside 1..256, M < 1). */
+et_status et_shard_bounds(const uint8_t* codes, int64_t n, int32_t M, int32_t G,
+                          int32_t K, int32_t* bounds);
+
+/* IVF shard plan (host only): whole inverted lists to G ranks by LPT --
+ * lists in decreasing size (ties: lower list first), each to the currently
+ * least-loaded rank (ties: lower rank).  list_sizes: HOST int64 [nlist];
+ * owner: HOST int32 [nlist] output.  Errors: ET_ERR_CONFIG. */
+et_status et_shard_lists(const int64_t* list_sizes, int32_t nlist, int32_t G, int32_t* owner);
+
 /* Naive ADC on the GPU (comparison kernel): out[q][slot] =
  * sum_m luts[q][m][codes[slot][m]], m ascending.  codes DEVICE [n][M]. */
 et_status et_flat_adc(const float* luts, int64_t Q, int32_t M, int32_t K,

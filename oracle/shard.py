@@ -18,15 +18,16 @@ from . import topk as _topk
 
 def shard_bounds(first_byte: np.ndarray, G: int, K: int = 256) -> np.ndarray:
     """G+1 byte boundaries b_0=0 <= ... <= b_G=K; shard r holds first bytes in
-    [b_r, b_{r+1})."""
-    hist = np.bincount(np.asarray(first_byte, dtype=np.int64), minlength=K)
-    below = np.concatenate(([0], np.cumsum(hist)))      # below[v] = #codes with byte < v
-    N = int(below[-1])
+    [b_r, b_{r+1}).  Written as the rule reads: for each r, walk v up from
+    0 until the number of codes whose first byte is < v reaches r*N/G."""
+    fb = [int(x) for x in np.asarray(first_byte).ravel()]
+    N = len(fb)
     b = [0]
     for r in range(1, G):
-        target = r * N / G
-        v = int(np.searchsorted(below, target, side="left"))
-        b.append(max(b[-1], min(v, K)))
+        v = 0
+        while v < K and sum(1 for x in fb if x < v) < r * N / G:
+            v += 1
+        b.append(max(b[-1], v))
     b.append(K)
     return np.array(b, dtype=np.int64)
 

@@ -70,6 +70,8 @@ SIGNATURES = [
     ("et_ivf_topk", C.c_int, [P, P, I64, I32, I32, P, P, P, P, SZ, P]),
     ("et_merge_topk", C.c_int, [P, P, I32, I64, I32, P, P, P]),
     ("et_flat_adc", C.c_int, [P, I64, I32, I32, P, I64, P, P]),
+    ("et_shard_bounds", C.c_int, [P, I64, I32, I32, I32, P]),
+    ("et_shard_lists", C.c_int, [P, I32, I32, P]),
 ]
 
 EXPORTED = [s[0] for s in SIGNATURES]

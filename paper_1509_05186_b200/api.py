@@ -329,3 +329,20 @@ def et_flat_adc(luts, codes, stream=None):
     out = torch.empty((Q, n), dtype=torch.float32, device=luts.device)
     check(_lib.load().et_flat_adc(_ptr(luts), Q, M, K, _ptr(codes), n, _ptr(out), _stream(stream)))
     return out
+
+
+def et_shard_bounds(codes, G: int, K: int = 256) -> np.ndarray:
+    """Host shard plan by first-level subtree: int32 [G+1] byte bounds."""
+    codes = _host(codes, np.uint8)
+    n, M = codes.shape if codes.ndim == 2 else (codes.shape[0], 1)
+    b = np.empty(G + 1, dtype=np.int32)
+    check(_lib.load().et_shard_bounds(_ptr(codes), n, M, G, K, _ptr(b)))
+    return b
+
+
+def et_shard_lists(list_sizes, G: int) -> np.ndarray:
+    """Host IVF shard plan (LPT on list size): int32 [nlist] owner rank."""
+    ls = _host(list_sizes, np.int64)
+    owner = np.empty(len(ls), dtype=np.int32)
+    check(_lib.load().et_shard_lists(_ptr(ls), len(ls), G, _ptr(owner)))
+    return owner

@@ -1037,6 +1037,43 @@ et_status et_merge_topk(const float* in_dist, const int32_t* in_ids, int32_t G, 
   ET_API_END
 }
 
+et_status et_shard_bounds(const uint8_t* codes, int64_t n, int32_t M, int32_t G, int32_t K, int32_t* bounds) {
+  ET_API_BEGIN
+  if (!bounds || (n > 0 && !codes)) fail(ET_ERR_CONFIG, "null argument");
+  if (G < 1 || K < 1 || K > 256 || M < 1 || n < 0) fail(ET_ERR_CONFIG, "bad G/K/M/n");
+  std::vector<int64_t> below(K + 1, 0);   // below[v] = #codes with byte 0 < v
+  for (int64_t i = 0; i < n; ++i) {
+    const int b = codes[(size_t)i * M];
+    if (b >= K) fail(ET_ERR_INVALID_CODE, "code byte >= K");
+    ++below[b + 1];
+  }
+  for (int v = 0; v < K; ++v) below[v + 1] += below[v];
+  bounds[0] = 0;
+  int v = 0;
+  for (int r = 1; r < G; ++r) {   // below[] is non-decreasing: the cut only moves right
+    while (v < K && (__int128)below[v] * G < (__int128)r * n) ++v;
+    bounds[r] = std::max(bounds[r - 1], v);
+  }
+  bounds[G] = K;
+  ET_API_END
+}
+
+et_status et_shard_lists(const int64_t* list_sizes, int32_t nlist, int32_t G, int32_t* owner) {
+  ET_API_BEGIN
+  if (!list_sizes || !owner) fail(ET_ERR_CONFIG, "null argument");
+  if (G < 1 || nlist < 1) fail(ET_ERR_CONFIG, "bad G/nlist");
+  std::vector<int32_t> order(nlist);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return list_sizes[a] > list_sizes[b]; });
+  std::vector<int64_t> load(G, 0);
+  for (int32_t c : order) {
+    const int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());   // first minimum
+    owner[c] = r;
+    load[r] += list_sizes[c];
+  }
+  ET_API_END
+}
+
 et_status et_flat_adc(const float* luts, int64_t Q, int32_t M, int32_t K, const uint8_t* codes, int64_t n,
                       float* out, void* stream) {
   ET_API_BEGIN

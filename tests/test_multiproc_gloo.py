@@ -65,8 +65,31 @@ def test_sharded_topk_over_gloo(tmp_path, world):
 
 
 def test_shard_bounds_match_oracle_rule():
+    """The product's C++ cut (et_shard_bounds) against the oracle's rule as
+    written (a plain loop over byte values), incl. skewed and empty shards."""
     from oracle import shard as oshard
-    from paper_1509_05186_b200 import shard, synth
-    for G in (1, 2, 4, 8):
-        fb = synth.random_codes(40 + G, 5000, 1, 256)[:, 0]
-        assert np.array_equal(shard.shard_bounds(fb, G), oshard.shard_bounds(fb, G))
+    from paper_1509_05186_b200 import api, build, synth
+    build.build()
+    for G in (1, 2, 3, 4, 8):
+        for codes in (synth.random_codes(40 + G, 3000, 2, 256),
+                      synth.random_codes(50 + G, 700, 3, 16),
+                      np.repeat(synth.random_codes(60 + G, 3, 2, 256), 200, axis=0)):   # 3 first bytes
+            K = 16 if codes.max() < 16 else 256
+            got = api.et_shard_bounds(codes, G, K)
+            assert np.array_equal(got, oshard.shard_bounds(codes[:, 0], G, K)), (G, K)
+
+
+def test_ivf_list_shard_plan_is_a_balanced_partition():
+    """LPT plan (et_shard_lists): every list owned by exactly one rank; the
+    load spread is at most the largest list (the greedy bound)."""
+    from paper_1509_05186_b200 import api, build
+    build.build()
+    r = np.random.default_rng(9)
+    for G in (1, 2, 3, 8):
+        sizes = r.integers(0, 40000, size=1024)
+        sizes[:4] = 0
+        owner = api.et_shard_lists(sizes, G)
+        assert owner.min() >= 0 and owner.max() < G
+        load = np.bincount(owner, weights=sizes, minlength=G)
+        assert load.sum() == sizes.sum()
+        assert load.max() - load.min() <= sizes.max()

@@ -1,4 +1,6 @@
 """Pins for oracle/eforest.py, topk.py, ivf.py, shard.py and the synth module."""
+import os
+
 import numpy as np
 import pytest
 
@@ -147,3 +149,86 @@ def test_synth_deterministic_and_random_access():
     c3 = synth.scaled(synth.CONFIGS["c3"], N=10)
     x = synth.base(c3)
     assert x.shape == (10, 960) and x.min() >= 0 and not np.array_equal(x, np.rint(x))
+
+
+# ------------------------------------------------------------------ ivf probe / assignment pins
+
+def _golden_probe():
+    cent, qv, exp = None, None, {}
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ivf_probe.txt")) as f:
+        for line in f:
+            line = line.split("#", 1)[0].split()
+            if not line:
+                continue
+            if line[0] == "centroids":
+                cent = np.array([[float(t)] for t in line[1:]], np.float32)
+            elif line[0] == "query":
+                qv = np.array([[float(line[1])]], np.float32)
+            elif line[0] == "expect":
+                exp[int(line[1][1:])] = [int(t) for t in line[2:]]
+    return cent, qv, exp
+
+
+def test_ivf_probe_golden_ties_to_lower_cell():
+    """Hand example (tests/golden/ivf_probe.txt): w < K' with exact distance
+    ties (cells 1/2 at 1, 3/4 at 4) resolving to the lower cell."""
+    cent, qv, exp = _golden_probe()
+    for w, cells in exp.items():
+        assert ivf.probe(qv, cent, w)[0].tolist() == cells, w
+
+
+def _brute_probe(qx, coarse, w):
+    """Pure-Python brute force: every distance by an explicit loop, then
+    Python's sort on (distance, cell) tuples."""
+    out = []
+    for q in qx:
+        d = []
+        for c, cc in enumerate(coarse):
+            s = 0.0
+            for a, b in zip(q.tolist(), cc.tolist()):
+                s += (a - b) * (a - b)
+            d.append((s, c))
+        out.append([c for _, c in sorted(d)[:w]])
+    return np.array(out)
+
+
+@pytest.mark.parametrize("seed,w", [(1, 1), (2, 3), (3, 7), (4, 16)])
+def test_ivf_probe_brute_force_and_nesting(seed, w):
+    r = np.random.default_rng(seed)
+    coarse = r.integers(0, 4, size=(16, 3)).astype(np.float32)   # small integers: many exact ties
+    qx = r.integers(0, 4, size=(9, 3)).astype(np.float32)
+    got = ivf.probe(qx, coarse, w)
+    assert np.array_equal(got, _brute_probe(qx, coarse, w))
+    # nesting: the w nearest are the first w of the w+1 nearest; w = K' is a permutation
+    if w < 16:
+        assert np.array_equal(ivf.probe(qx, coarse, w + 1)[:, :w], got)
+    allp = ivf.probe(qx, coarse, 16)
+    assert all(sorted(row) == list(range(16)) for row in allp.tolist())
+
+
+def test_encode_ivf_assignment_and_residual_codes_pinned():
+    """encode_ivf: (a) vectors built as coarse centroid + a codeword
+    concatenation, with well-separated centroids, get exactly that cell and
+    re-encode to exactly those codewords (SPEC.md:369 'each residual code
+    re-encodes to itself'); (b) K' = 1 degenerates to PQ of x - centroid
+    (SPEC.md:367); (c) ties in the coarse assignment go to the lower cell."""
+    r = np.random.default_rng(11)
+    M, K, s, nl = 4, 8, 2, 5
+    coarse = (np.arange(nl, dtype=np.float32)[:, None] * 1000.0) * np.ones((1, M * s), np.float32)
+    cbs = r.integers(-3, 4, size=(M, K, s)).astype(np.float32)
+    # make the codewords of each subspace distinct so the re-encode is unique
+    cbs[:, :, 0] = np.arange(K, dtype=np.float32)[None, :] * 10.0
+    cell = r.integers(0, nl, size=40)
+    code = r.integers(0, K, size=(40, M))
+    X = coarse[cell] + np.concatenate([cbs[m][code[:, m]] for m in range(M)], axis=1)
+    ix = ivf.encode_ivf(X.astype(np.float32), coarse, cbs)
+    assert ix.assign.tolist() == cell.tolist()
+    assert np.array_equal(ix.codes, code.astype(np.uint8))
+    # (b) one cell
+    c1 = X.mean(0, keepdims=True).astype(np.float32)
+    ix1 = ivf.encode_ivf(X.astype(np.float32), c1, cbs)
+    assert np.all(ix1.assign == 0)
+    assert np.array_equal(ix1.codes, pq.encode(cbs, X.astype(np.float64) - c1.astype(np.float64)))
+    # (c) a point equidistant from cells 1 and 2 -> cell 1
+    mid = ((coarse[1] + coarse[2]) / 2)[None, :]
+    assert ivf.encode_ivf(mid, coarse, cbs).assign.tolist() == [1]
