@@ -222,6 +222,9 @@ et_status et_merge_topk(const float* in_dist, const int32_t* in_ids, int32_t G,
  * Errors: ET_ERR_CONFIG (null pointer, G < 1, K outside 1..256, M < 1). */
 et_status et_shard_bounds(const uint8_t* codes, int64_t n, int32_t M, int32_t G,
                           int32_t K, int32_t* bounds);
+/* The same cut from a first-byte histogram: hist HOST int64 [K] (e.g. summed
+ * over ranks that each hold part of the codes). */
+et_status et_shard_bounds_hist(const int64_t* hist, int32_t K, int32_t G, int32_t* bounds);
 
 /* IVF shard plan (host only): whole inverted lists to G ranks by LPT --
  * lists in decreasing size (ties: lower list first), each to the currently

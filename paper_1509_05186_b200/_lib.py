@@ -72,6 +72,7 @@ SIGNATURES = [
     ("et_flat_adc", C.c_int, [P, I64, I32, I32, P, I64, P, P]),
     ("et_shard_bounds", C.c_int, [P, I64, I32, I32, I32, P]),
     ("et_shard_lists", C.c_int, [P, I32, I32, P]),
+    ("et_shard_bounds_hist", C.c_int, [P, I32, I32, P]),
 ]
 
 EXPORTED = [s[0] for s in SIGNATURES]

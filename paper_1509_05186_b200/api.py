@@ -346,3 +346,11 @@ def et_shard_lists(list_sizes, G: int) -> np.ndarray:
     owner = np.empty(len(ls), dtype=np.int32)
     check(_lib.load().et_shard_lists(_ptr(ls), len(ls), G, _ptr(owner)))
     return owner
+
+
+def et_shard_bounds_hist(hist, G: int) -> np.ndarray:
+    """Shard bounds from a first-byte histogram (int64 [K])."""
+    h = _host(hist, np.int64)
+    b = np.empty(G + 1, dtype=np.int32)
+    check(_lib.load().et_shard_bounds_hist(_ptr(h), len(h), G, _ptr(b)))
+    return b

@@ -1037,17 +1037,14 @@ et_status et_merge_topk(const float* in_dist, const int32_t* in_ids, int32_t G, 
   ET_API_END
 }
 
-et_status et_shard_bounds(const uint8_t* codes, int64_t n, int32_t M, int32_t G, int32_t K, int32_t* bounds) {
-  ET_API_BEGIN
-  if (!bounds || (n > 0 && !codes)) fail(ET_ERR_CONFIG, "null argument");
-  if (G < 1 || K < 1 || K > 256 || M < 1 || n < 0) fail(ET_ERR_CONFIG, "bad G/K/M/n");
+// The cut rule of et_shard_bounds on a first-byte histogram (shared by both entry points).
+static void shard_cut(const int64_t* hist, int K, int G, int32_t* bounds) {
   std::vector<int64_t> below(K + 1, 0);   // below[v] = #codes with byte 0 < v
-  for (int64_t i = 0; i < n; ++i) {
-    const int b = codes[(size_t)i * M];
-    if (b >= K) fail(ET_ERR_INVALID_CODE, "code byte >= K");
-    ++below[b + 1];
+  for (int v = 0; v < K; ++v) {
+    if (hist[v] < 0) fail(ET_ERR_CONFIG, "negative histogram count");
+    below[v + 1] = below[v] + hist[v];
   }
-  for (int v = 0; v < K; ++v) below[v + 1] += below[v];
+  const int64_t n = below[K];
   bounds[0] = 0;
   int v = 0;
   for (int r = 1; r < G; ++r) {   // below[] is non-decreasing: the cut only moves right
@@ -1055,6 +1052,27 @@ et_status et_shard_bounds(const uint8_t* codes, int64_t n, int32_t M, int32_t G,
     bounds[r] = std::max(bounds[r - 1], v);
   }
   bounds[G] = K;
+}
+
+et_status et_shard_bounds(const uint8_t* codes, int64_t n, int32_t M, int32_t G, int32_t K, int32_t* bounds) {
+  ET_API_BEGIN
+  if (!bounds || (n > 0 && !codes)) fail(ET_ERR_CONFIG, "null argument");
+  if (G < 1 || K < 1 || K > 256 || M < 1 || n < 0) fail(ET_ERR_CONFIG, "bad G/K/M/n");
+  std::vector<int64_t> hist(K, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    const int b = codes[(size_t)i * M];
+    if (b >= K) fail(ET_ERR_INVALID_CODE, "code byte >= K");
+    ++hist[b];
+  }
+  shard_cut(hist.data(), K, G, bounds);
+  ET_API_END
+}
+
+et_status et_shard_bounds_hist(const int64_t* hist, int32_t K, int32_t G, int32_t* bounds) {
+  ET_API_BEGIN
+  if (!hist || !bounds) fail(ET_ERR_CONFIG, "null argument");
+  if (G < 1 || K < 1 || K > 256) fail(ET_ERR_CONFIG, "bad G/K");
+  shard_cut(hist, K, G, bounds);
   ET_API_END
 }
 

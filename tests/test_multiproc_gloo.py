@@ -93,3 +93,60 @@ def test_ivf_list_shard_plan_is_a_balanced_partition():
         load = np.bincount(owner, weights=sizes, minlength=G)
         assert load.sum() == sizes.sum()
         assert load.max() - load.min() <= sizes.max()
+
+
+def _bench_dry(config, gpus, n=20_000, q=6):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    for v in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(v, None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(gpus), "--config", config,
+                        "--dry-run", "bench_dry_backend:Backend", "--dry-n", str(n), "--dry-q", str(q)],
+                       capture_output=True, text=True, env=env, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("config,mode", [("c5", "db"), ("c4", "lists")])
+def test_bench_dry_run_two_ranks_equals_oracle_global_topk(config, mode):
+    """bench.py --gpus 2 (self-launched under torchrun, gloo): each rank
+    generates half the base, the rows are exchanged by first byte (db) or by
+    list owner (lists), per-shard top-k lists are all-gathered and merged --
+    and the merged lists equal the oracle's global top-k on the whole base."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from bench_dry_backend import Backend
+    from paper_1509_05186_b200 import synth
+    out2 = _bench_dry(config, 2)
+    assert out2["world"] == 2 and out2["mode"] == mode
+    # the single-process reference: the same recipe on one rank (no sharding)
+    be = Backend()
+    over = dict(N=20_000, Q=6, n_train=2000, lloyd_iters=3)
+    cfg = synth.scaled(synth.CONFIGS[config], **over)
+    if cfg.ivf_nlist:
+        cfg = synth.scaled(cfg, ivf_nlist=16, n_coarse_train=2000)
+    means = synth.mixture_means(cfg)
+    st = {"qx": synth.queries(cfg, means=means), "ids": np.arange(cfg.N)}
+    if cfg.ivf_nlist:
+        co = be.train_coarse(synth.coarse_train(cfg, means=means), cfg.ivf_nlist, cfg.lloyd_iters,
+                             synth.kmeanspp_seed(cfg, 1))
+        rt = synth.resid_train(cfg, means=means)
+        a = be.assign(co, rt)
+        cb = be.train_codebooks((rt - co[a]).astype(np.float32), cfg.M, cfg.K, cfg.lloyd_iters,
+                                synth.kmeanspp_seed(cfg, 2))
+        st["codes"], st["cells"] = be.encode(cb, synth.base(cfg, means=means), co)
+        st["coarse"] = co
+    else:
+        cb = be.train_codebooks(synth.train(cfg, means=means), cfg.M, cfg.K, cfg.lloyd_iters,
+                                synth.kmeanspp_seed(cfg))
+        st["codes"], _ = be.encode(cb, synth.base(cfg, means=means))
+    st["cb"] = cb
+    D, I = be.topk(cfg, st)
+    assert out2["n_local"] < cfg.N
+    assert np.array_equal(np.array(out2["ids"]), I)
+    assert np.array_equal(np.array(out2["dist"]), D)
