@@ -54,7 +54,11 @@ def check_topk(gd, gi, cb, qx, codes, k, qidx, ids_map=None, rtol=RTOL):
         inv[ids_all] = np.arange(N)
     for q in qidx:
         full = oracle_dist(cb, qx[q], codes)
-        od, oi = otopk.topk(full[None, :], ids_all, k)
+        # the oracle's full sort on the exact superset {distance <= k-th smallest}
+        kk = min(k, N)
+        kth = np.partition(full, kk - 1)[kk - 1]
+        sel = np.flatnonzero(full <= kth)
+        od, oi = otopk.topk(full[sel][None, :], ids_all[sel], k)
         od, oi = od[0], oi[0]
         g_d = gd[q].astype(np.float64)
         g_i = gi[q].astype(np.int64)

@@ -70,7 +70,7 @@ def c5_full():
                         synth.kmeanspp_seed(cfg))
     sys.path.insert(0, ROOT)
     import bench   # the bench's generator + et_encode pipeline (process pool)
-    codes = bench.gen_base_encode(cfg, dev(cb), means, torch.device("cuda", 0))
+    codes, _ = bench.gen_encode_range(cfg, {}, bench.CudaBackend(torch.device("cuda", 0)), cb, means, 0, cfg.N)
     qx = synth.queries(cfg, means=means)
     return cfg, cb, codes, qx, means
 
@@ -118,3 +118,105 @@ def test_c5_full_size_topk_sampled(c5_full):
         mism = g_i != oi
         if mism.any():
             assert np.all(np.abs(truth[mism] - od[mism]) <= RTOL * od[mism]), q
+
+
+# --------------------------------------------------------------------------- c4 at full size
+
+@pytest.fixture(scope="module")
+def c4_full():
+    """BASELINE config 4 at full size: coarse quantizer (K' = 1024) and the
+    residual codebook trained by the ORACLE (k-means++ + 25 Lloyd); the 10^7
+    base vectors assigned and encoded by et_assign / et_encode (reading C4b:
+    the oracle cannot encode 10^7 x 1024 in test time) -- pinned below on
+    sampled blocks against oracle assign + encode."""
+    cfg = synth.CONFIGS["c4"]
+    means = synth.mixture_means(cfg)
+    coarse, _ = pq.kmeans(synth.coarse_train(cfg, means=means), cfg.ivf_nlist, cfg.lloyd_iters,
+                          synth.kmeanspp_seed(cfg, 1))
+    coarse = coarse.astype(np.float32)
+    rt = synth.resid_train(cfg, means=means)
+    a = pq.assign(rt, coarse)
+    cb, _ = pq.train_pq((rt.astype(np.float64) - coarse[a]).astype(np.float32), cfg.M, cfg.K, cfg.lloyd_iters,
+                        synth.kmeanspp_seed(cfg, 2))
+    cd, cbd = dev(coarse), dev(cb)
+    codes = np.empty((cfg.N, cfg.M), np.uint8)
+    cells = np.empty(cfg.N, np.int32)
+    sys.path.insert(0, ROOT)
+    import bench
+    import multiprocessing as mp
+    jobs = [("c4", {}, s, min(1 << 18, cfg.N - s)) for s in range(0, cfg.N, 1 << 18)]
+    with mp.get_context("spawn").Pool(max(1, min(32, (os.cpu_count() or 2) - 1)), initializer=bench._gen_init,
+                                      initargs=("c4", {})) as pool:
+        for s, x in pool.imap(bench._gen_chunk, jobs, chunksize=1):
+            xd = dev(x)
+            asg = api.et_assign(cd, xd)
+            codes[s:s + len(x)] = api.et_encode(cbd, xd, centroids=cd, assign=asg).cpu().numpy()
+            cells[s:s + len(x)] = asg.cpu().numpy()
+    return cfg, coarse, cb, codes, cells, synth.queries(cfg, means=means), means
+
+
+def test_c4_assign_encode_match_oracle_on_sampled_blocks(c4_full):
+    cfg, coarse, cb, codes, cells, qx, means = c4_full
+    rng = np.random.default_rng(4)
+    s = cfg.d // cfg.M
+    for b in rng.choice(cfg.N // synth.BLOCK, 2, replace=False):
+        lo = int(b) * synth.BLOCK
+        X = synth.base(cfg, lo, synth.BLOCK, means=means)
+        oa = pq.assign(X, coarse)
+        diff = np.flatnonzero(oa != cells[lo:lo + synth.BLOCK])
+        for r in diff:   # coarse near ties only
+            dd = pq.sqdist_direct(X[r:r + 1], coarse)[0]
+            x1, x2 = dd[oa[r]], dd[cells[lo + r]]
+            assert abs(x1 - x2) <= 1e-5 * max(x1, x2)
+        R = X.astype(np.float64) - coarse[cells[lo:lo + synth.BLOCK]].astype(np.float64)
+        ref = pq.encode(cb, R)
+        got = codes[lo:lo + synth.BLOCK]
+        bad = np.argwhere(got != ref)
+        for (r, m) in bad:
+            dd = pq.sqdist_direct(R[r:r + 1, m * s:(m + 1) * s], cb[m])[0]
+            x1, x2 = dd[got[r, m]], dd[ref[r, m]]
+            assert abs(x1 - x2) <= 1e-5 * max(x1, x2)
+        assert len(diff) <= 64 and len(bad) <= 64
+
+
+def test_c4_full_size_ivf_topk_sampled(c4_full):
+    """N = 10^7, K' = 1024, w = 8, Q = 10^4, top-100 in the launch bench.py
+    times; 24 sampled queries vs the oracle's probe (fp64) and exact residual
+    ADC64 top-k over the probed lists (C6 near-tie rule for the probes)."""
+    from oracle import ivf as oivf
+    cfg, coarse, cb, codes, cells, qx, means = c4_full
+    ix = api.Index.et_build_ivf(codes, cells, coarse, cb)
+    d, i, pr = ix.et_ivf_topk(dev(qx), nprobe=cfg.ivf_nprobe, k=cfg.topk, return_probes=True)
+    torch.cuda.synchronize()
+    d, i, pr = d.cpu().numpy(), i.cpu().numpy(), pr.cpu().numpy()
+    order = np.argsort(cells, kind="stable")
+    starts = np.searchsorted(cells[order], np.arange(cfg.ivf_nlist + 1))
+    rng = np.random.default_rng(44)
+    sample = sorted(set([0, cfg.Q - 1] + rng.choice(cfg.Q, 22, replace=False).tolist()))
+    oprobe = oivf.probe(qx[sample], coarse, cfg.ivf_nprobe)
+    for j, q in enumerate(sample):
+        if not np.array_equal(np.sort(pr[q]), np.sort(oprobe[j])):
+            cd = pq.sqdist_direct(qx[q:q + 1], coarse)[0]
+            kth = np.sort(cd)[cfg.ivf_nprobe - 1]
+            for c in set(pr[q]) ^ set(oprobe[j]):
+                assert abs(cd[c] - kth) <= 1e-5 * kth, (q, c)
+        members, dists = [], []
+        for c in pr[q]:
+            m = order[starts[c]:starts[c + 1]]
+            if len(m):
+                r = qx[q].astype(np.float64) - coarse[c].astype(np.float64)
+                dists.append(pq.adc(pq.lut64(cb, r[None]), codes[m])[0])
+                members.append(m)
+        full, ids = np.concatenate(dists), np.concatenate(members)
+        od, oi = otopk.topk(full[None], ids, cfg.topk)
+        od, oi = od[0], oi[0]
+        nv = int((oi >= 0).sum())
+        g_d, g_i = d[q].astype(np.float64), i[q].astype(np.int64)
+        assert int((g_i >= 0).sum()) == nv and len(np.unique(g_i[:nv])) == nv
+        pos = {int(x): t for t, x in enumerate(ids)}
+        truth = full[[pos[int(x)] for x in g_i[:nv]]]
+        assert np.all(np.abs(g_d[:nv] - truth) <= RTOL * np.maximum(truth, 1e-30)), q
+        assert np.all(np.abs(g_d[:nv] - od[:nv]) <= RTOL * np.maximum(od[:nv], 1e-30)), q
+        mism = g_i[:nv] != oi[:nv]
+        if mism.any():
+            assert np.all(np.abs(truth[mism] - od[:nv][mism]) <= RTOL * od[:nv][mism]), q

@@ -112,13 +112,13 @@ def c2():
 
 def test_c2_topk_full_size_sampled(c2):
     """BASELINE config 2 at full size (N=1e6, Q=1e4, top-100), in the launch
-    configuration bench.py times; 40 sampled queries vs the oracle."""
+    configuration bench.py times; 200 sampled queries vs the oracle."""
     cfg, cb, codes, qx, X = c2
     ix = api.Index.et_build_etree(codes)
     d, i = ix.et_etree_topk(100, queries=dev(qx), codebooks=dev(cb))
     torch.cuda.synchronize()
     rng = np.random.default_rng(7)
-    sample = sorted(set([0, cfg.Q - 1] + rng.choice(cfg.Q, 38, replace=False).tolist()))
+    sample = sorted(set([0, cfg.Q - 1] + rng.choice(cfg.Q, 198, replace=False).tolist()))
     check_topk(d.cpu().numpy(), i.cpu().numpy(), cb, qx, codes, 100, sample)
     # property at any size: rows sorted by (dist, id), ids in range, distances
     # equal the oracle ADC64 of the returned ids for every query
@@ -264,13 +264,12 @@ def test_forest_T1_equals_tree_and_split_invariance(c1):
 def test_logical_shards_merge_equals_single(c1):
     """shards of first-level subtrees; per-shard top-k merged with
     K7 equals the single-index top-k exactly (same sums, same order)."""
-    from oracle import shard as oshard
     cfg, cb, codes, qx, X = c1
     k = 100
     one = api.Index.et_build_etree(codes)
     d1, i1 = one.et_etree_topk(k, queries=dev(qx), codebooks=dev(cb))
     for G in (2, 3, 8):
-        b = oshard.shard_bounds(codes[:, 0], G)
+        b = api.et_shard_bounds(codes, G)   # the product's cut (host C++)
         ds, is_ = [], []
         for r in range(G):
             m = np.flatnonzero((codes[:, 0] >= b[r]) & (codes[:, 0] < b[r + 1]))
@@ -285,6 +284,8 @@ def test_logical_shards_merge_equals_single(c1):
         md, mi = api.et_merge_topk(torch.stack(ds), torch.stack(is_))
         torch.cuda.synchronize()
         assert torch.equal(mi, i1) and torch.equal(md, d1), G
+        # and against the oracle's global top-k (not only the single GPU index)
+        check_topk(md.cpu().numpy(), mi.cpu().numpy(), cb, qx, codes, k, range(cfg.Q))
 
 
 # --------------------------------------------------------------------------- PQ support kernels

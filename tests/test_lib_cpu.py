@@ -91,3 +91,26 @@ def test_host_build_uniform_u1m_scale(lib):
     sc, _ = oetree.sort_codes(codes)
     r = oetree.tree_stats_def(sc)
     assert (g["L1"], g["L2"], g["total_postfix"]) == (r.L1, r.L2, r.total_postfix)
+
+
+@pytest.mark.parametrize("seed,N,M,K,nd,split", [c for c in CASES if len(c[5]) > 2 and c[5][-1] <= 8])
+def test_fused_forest_scan_lookups(lib, seed, N, M, K, nd, split):
+    """Fused E-Forest (M <= 8): the scan's lookups per query
+    are each tree's Distance Context run along the distinct full codes in
+    lexicographic order -- sum over tuples of sum over trees of
+    (tree width - LCP with the previous tuple over that tree's bytes).  For
+    T = 1 this is exactly L1 + L2 + postfix."""
+    codes = synth.random_codes(seed, N, M, K, nd)
+    U = np.unique(codes, axis=0)          # distinct full codes, lexicographic
+    exp = 0
+    for i in range(len(U)):
+        for a, b in zip(split, split[1:]):
+            l = 0
+            if i:
+                while a + l < b and U[i, a + l] == U[i - 1, a + l]:
+                    l += 1
+            exp += (b - a) - l
+    got = api.et_build_stats(codes, split=list(split), K=K)
+    assert all(g["scan_lookups"] == exp for g in got)
+    t1 = api.et_build_stats(codes, K=K)[0]
+    assert t1["scan_lookups"] == t1["lookups"]
