@@ -69,6 +69,9 @@ typedef struct et_tree_stats {
   int64_t paper_bytes;     /* 4N + 2(L1 + L2_records) + chained postfix bytes   */
   int64_t device_bytes;    /* bytes of this tree's device layout         */
   int64_t groups;          /* id groups (leaves, or forest tuples) -- index-wide        */
+  int64_t scan_lookups;    /* index-wide: table lookups per query of the GPU scan before
+                              pruning (E-Tree: = lookups; fused E-Forest: each tree's
+                              Distance Context over the tuple sequence) */
 } et_tree_stats;
 
 const char* et_last_error(void);

@@ -29,7 +29,7 @@ class TreeStats(C.Structure):
         ("N", C.c_int64), ("M", C.c_int32), ("layer0", C.c_int32),
         ("L1", C.c_int64), ("L2", C.c_int64), ("total_postfix", C.c_int64),
         ("lookups", C.c_int64), ("L2_records", C.c_int64), ("paper_bytes", C.c_int64),
-        ("device_bytes", C.c_int64), ("groups", C.c_int64),
+        ("device_bytes", C.c_int64), ("groups", C.c_int64), ("scan_lookups", C.c_int64),
     ]
 
     def as_dict(self):

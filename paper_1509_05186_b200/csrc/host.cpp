@@ -15,6 +15,7 @@
 #include <mutex>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -115,6 +116,7 @@ struct DevBuf {
     cuda_check(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice), "upload(index)");
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+  void reset() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
 };
 
 enum Kind { kTree = 0, kIvf = 1, kFlat = 2 };
@@ -139,6 +141,8 @@ struct et_index {
   int device = 0;
   et_tree_stats stats[et::kMaxTrees] = {};
   et::DevBuf code[et::kMaxTrees], lcp[et::kMaxTrees];
+  bool fused = false;                // forest with M <= 8: one scan over masked tuple records
+  et::DevBuf fused_rec;
   int64_t n_leaves[et::kMaxTrees] = {};
   et::DevBuf group_off, ids, group_mult, group_minid, slot2group;
   et::DevBuf t0_tup_off, tup_leaf[et::kMaxTrees];
@@ -280,9 +284,10 @@ static void upload_groups(et_index* ix, const Groups& g, const std::vector<uint3
 // half-words; half-word l = the pre-swizzled byte offset of table entry
 // (l, k = code byte l) inside that level's 32 KB shared-memory table,
 // (k << 7) | ((k & 31) << 2), so a lookup is one XOR with the lane's offset.
-// Level 0 of an 8-level tree (held in TMEM) stores the column k with the LCP
-// with the previous leaf in bits 8..11 and floor(log2(multiplicity)) in bits
-// 12..15; shorter trees keep both in half-word 7 (bits 0..3, 4..7).
+// Levels 0 and 1 of an 8-level tree (held in TMEM) store the column k; half-
+// word 0 adds the LCP with the previous leaf in bits 8..11 and
+// floor(log2(multiplicity)) in bits 12..15; shorter trees keep both in
+// half-word 7 (bits 0..3, 4..7).
 static std::vector<uint4> make_records(const HostTree& h) {
   const int MT = h.MT;
   std::vector<uint4> rec(h.code.size());
@@ -290,7 +295,7 @@ static std::vector<uint4> make_records(const HostTree& h) {
     uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int l = 0; l < MT; ++l) {
       const uint32_t k = (uint32_t)((h.code[i] >> (8 * l)) & 255u);
-      w[l] = (MT == 8 && l == 0) ? k : ((k << 7) | ((k & 31u) << 2));
+      w[l] = (MT == 8 && l < kTmemLevels) ? k : ((k << 7) | ((k & 31u) << 2));   // TMEM levels: the column
     }
     const uint32_t lcp = (i < h.lcp.size()) ? h.lcp[i] : 0u;
     const uint64_t mu = (i < h.mult.size()) ? h.mult[i] : 1;
@@ -301,6 +306,43 @@ static std::vector<uint4> make_records(const HostTree& h) {
     rec[i] = make_uint4(w[0] | (w[1] << 16), w[2] | (w[3] << 16), w[4] | (w[5] << 16), w[6] | (w[7] << 16));
   }
   return rec;
+}
+
+// Fused E-Forest records (M <= 8): one record per tuple
+// (distinct full code, in lexicographic order) = the single-tree record of
+// its full code whose LCP field is an 8-bit lookup mask: bit l is set iff
+// l - split[u] >= LCP(tuple t-1, tuple t) over tree u's bytes, u the tree of
+// level l.  Each tree's Distance Context then runs along the tuple
+// sequence and the per-tree partials are summed in tree order (A13).
+static int64_t build_fused(et_index* ix, const uint8_t* codes, const Groups& g, int M, int T, const int32_t* split) {
+  const size_t G = g.off.size() - 1;
+  std::vector<uint4> rec(G);
+  int64_t look = 0;
+  for (size_t j = 0; j < G; ++j) {
+    const uint8_t* row = codes + (size_t)g.first[j] * M;
+    const uint8_t* prev = j ? codes + (size_t)g.first[j - 1] * M : nullptr;
+    uint32_t mask = 0;
+    for (int u = 0; u < T; ++u) {
+      int l = 0;
+      if (prev) while (split[u] + l < split[u + 1] && row[split[u] + l] == prev[split[u] + l]) ++l;
+      for (int b = split[u] + l; b < split[u + 1]; ++b) mask |= 1u << b;
+    }
+    look += __builtin_popcount(mask);
+    const uint64_t mu = g.off[j + 1] - g.off[j];
+    uint32_t mb = 0;
+    while (mb < 15 && (2ull << mb) <= mu) ++mb;
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int l = 0; l < M; ++l) {
+      const uint32_t k = row[l];
+      w[l] = (M == 8 && l < kTmemLevels) ? k : ((k << 7) | ((k & 31u) << 2));
+    }
+    if (M == 8) { w[0] |= mask << 8; w[1] |= mb << 8; }
+    else w[7] = mask | (mb << 8);
+    rec[j] = make_uint4(w[0] | (w[1] << 16), w[2] | (w[3] << 16), w[4] | (w[5] << 16), w[6] | (w[7] << 16));
+  }
+  ix->fused = true;
+  ix->fused_rec.upload(rec);
+  return look;
 }
 
 static void finish_tree(et_index* ix, int t, HostTree& h) {
@@ -424,7 +466,12 @@ static et_index* build_forest(const uint8_t* codes_in, const int32_t* ids, int64
     finish_tree(ix.get(), t, h);
     ix->tup_leaf[t].upload(tup_leaf);
   }
-  for (int t = 0; t < T; ++t) ix->stats[t].groups = (int64_t)G;
+  int64_t scan_look = (int64_t)look;
+  if (T > 1 && M <= kMaxMT) {   // fused forest: one masked scan over the tuples
+    scan_look = build_fused(ix.get(), codes, g, M, T, split);
+    look = (double)scan_look;
+  }
+  for (int t = 0; t < T; ++t) { ix->stats[t].groups = (int64_t)G; ix->stats[t].scan_lookups = scan_look; }
   ix->lookups_per_query = look;
   return ix.release();
 }
@@ -450,6 +497,7 @@ static et_index* build_flat(const uint8_t* codes, const int32_t* ids, int64_t n,
   h.st.N = n; h.st.M = M; h.st.L2 = n; h.st.lookups = n * M; h.st.device_bytes = n * 16;
   h.st.L2_records = n; h.st.total_postfix = n * (M - 1); h.st.paper_bytes = 4 * n + n * M;
   finish_tree(ix.get(), 0, h);
+  ix->stats[0].scan_lookups = n * M;
   Groups g;
   g.off.resize(n + 1);
   g.ids.resize(n);
@@ -531,6 +579,7 @@ static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t 
   ix->n_leaves[0] = (int64_t)h.code.size();
   ix->code[0].upload(make_records(h));
   ix->lcp[0].upload(h.lcp);
+  tot.scan_lookups = tot.lookups;
   ix->stats[0] = tot;
   ix->list_leaf_off_d.upload(ix->list_leaf_off);
   ix->coarse.upload_raw(coarse, (size_t)nlist * d * 4);
@@ -566,11 +615,14 @@ struct Plan {
   int64_t part_base[kMaxTrees] = {};
 };
 
-static int topk_B(int k) { return ((2 * k + 64 + 31) / 32) * 32; }
+// candidate buffer per (unit, warp, lane): k survivors of a refresh + ties, plus
+// one batch of emissions (kBatchEmit) before the next buffer check
+static int topk_B(int k) { return ((2 * k + kBatchEmit + 31) / 32) * 32; }
 
 static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   Plan pl;
   for (int t = 0; t < ix->T; ++t) pl.MTmax = std::max(pl.MTmax, ix->stats[t].M);
+  if (ix->fused) pl.MTmax = ix->M;   // one scan over all M levels
   pl.lut0 = (pl.MTmax == 8);
   const int64_t base = (Q + 31) / 32;
   // Cost model per unit (cycles of one SM): tables ~ nq * K * d * 2 / 128 * 1.25
@@ -581,7 +633,7 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   const double look = std::max(1.0, ix->lookups_per_query);
   double best = 1e300;
   const int64_t cand_chunks[2] = {base, std::min<int64_t>(Q, ((base + nsm - 1) / nsm) * nsm)};
-  const int smax = (ix->T > 1) ? 1 : 64;
+  const int smax = (ix->T > 1 && !ix->fused) ? 1 : 64;
   for (int ci = 0; ci < 2; ++ci) {
     const int64_t nc = std::max<int64_t>(1, cand_chunks[ci]);
     const double nq = std::min<double>(32.0, std::ceil((double)Q / nc));
@@ -597,7 +649,7 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   pl.n_units = pl.n_chunks * pl.S;
   pl.B = topk_B(std::max(1, k));
   int64_t off = 0;
-  if (ix->T > 1)   // forests: per-leaf partials of every tree (the join reads them)
+  if (ix->T > 1 && !ix->fused)   // joined forests: per-leaf partials of every tree (the join reads them)
     for (int t = 0; t < ix->T; ++t) { pl.part_base[t] = off; off += ix->n_leaves[t] * 32; }
   pl.part_stride = off;
   return pl;
@@ -640,7 +692,7 @@ static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool 
   w.chunk_q = c.take<int>((size_t)pl.n_chunks * 32);
   w.qslot_off = c.take<int>(Q + 1);
   w.qslot = c.take<int>((size_t)Q * slots_per_q);
-  w.lut0 = pl.lut0 ? c.take<float>((size_t)pl.n_units * 256 * 32) : nullptr;
+  w.lut0 = pl.lut0 ? c.take<float>((size_t)pl.n_units * kTmemLevels * 256 * 32) : nullptr;
   w.partials = pl.part_stride ? c.take<float>((size_t)pl.n_units * pl.part_stride) : nullptr;
   if (full) {
     w.leafdist = c.take<float>((size_t)pl.n_chunks * ix->n_groups * 32);
@@ -688,8 +740,19 @@ static void fill_scan_common(ScanParams& sp, const et_index* ix, const Plan& pl)
   sp.M = ix->M; sp.K = ix->K;
   sp.layer_sub = ix->layer_sub_d.as<int>();
   for (int l = 0; l < ix->M && l < kMaxTrees * kMaxMT; ++l) sp.lsub[l] = ix->layer_sub[l];
-  sp.T = ix->T;
-  for (int t = 0; t < ix->T; ++t) {
+  if (ix->fused) {   // the forest's tuples scanned as one masked tree over all M levels
+    sp.T = 1;
+    sp.masked = 1;
+    sp.fsplit = 0;
+    for (int t = 1; t < ix->T; ++t) sp.fsplit |= 1u << ix->split[t];
+    sp.tree[0].MT = ix->M;
+    sp.tree[0].layer0 = 0;
+    sp.tree[0].n_leaves = ix->n_groups;
+    sp.tree[0].rec = ix->fused_rec.as<uint4>();
+  } else {
+    sp.T = ix->T;
+  }
+  for (int t = 0; t < ix->T && !ix->fused; ++t) {
     sp.tree[t].MT = ix->stats[t].M;
     sp.tree[t].layer0 = ix->split[t];
     sp.tree[t].n_leaves = ix->n_leaves[t];

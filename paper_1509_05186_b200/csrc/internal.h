@@ -7,13 +7,15 @@
 
 namespace et {
 
-constexpr int kWarps = 16;                 // warps per scan CTA (1 CTA / SM: the tables fill smem)
+constexpr int kWarps = 8;                  // warps per scan CTA (1 CTA / SM: the tables fill smem; 255 registers)
 constexpr int kThreads = kWarps * 32;
 constexpr int kMaxTrees = 4;               // E-Forest trees supported by one index
 constexpr int kMaxMT = 8;                  // levels (code bytes) per tree on the GPU
 constexpr int kKMax = 256;                 // codewords per subspace (one byte)
 constexpr int kTopkMax = 256;              // largest k of the fused top-k
 constexpr int kFinWarps = 8;               // warps per finalize CTA
+constexpr int kStreams = 4;                // lockstep leaf streams per scan warp (8 warps: 32 chains per SM)
+constexpr int kBatchEmit = 32 * kStreams;  // candidates a lane can append between two buffer checks
 
 // One tree of the device layout ("leaf-major HMS"): the leaves in
 // depth-first (= lexicographic) order, each with its full projected code and
@@ -99,7 +101,30 @@ struct ScanParams {
   int qthr_shared = 0;                // several units per query (S > 1, IVF): share during the scan
   int vec4 = 1;                       // query/codebook rows 16-byte aligned
   int compact = 0;                    // merge each lane's 16 per-warp lists at the end (long lists)
+  // ---- fused E-Forest (M <= 8) ----
+  int masked = 0;                     // records carry a per-level lookup mask (fused forest tuple records)
+  uint32_t fsplit = 0;                // bit l set: level l starts a forest tree (partials summed in tree order)
 };
+
+// Shared-memory layout of the scan kernel (byte offsets from the dynamic
+// shared-memory base).  8-level trees keep levels 0 and 1 in TMEM and levels
+// 2..7 in six 32 KB regions, and stage the chunk's query sub-vectors of all 8
+// levels in their own area; shorter trees keep every level in shared memory.
+constexpr int kTmemLevels = 2;             // levels of an 8-level tree held in TMEM
+struct ScanSmem { uint32_t levels, big_stage, thr, qidx, stage, tmem_slot, total; };
+__host__ __device__ inline ScanSmem scan_smem(int MTmax) {
+  ScanSmem L{};
+  L.levels = (MTmax == 8) ? 8 - kTmemLevels : (uint32_t)MTmax;
+  uint32_t off = L.levels * 32768u;
+  L.big_stage = off;
+  if (MTmax == 8) off += 8u * 16u * 128u;   // [level][query pair][dim][2] fp32
+  L.thr = off; off += 128u;
+  L.qidx = off; off += 128u;
+  L.stage = off; off += 32u * 16u * 4u;
+  L.tmem_slot = off; off += 16u;
+  L.total = off;
+  return L;
+}
 
 // ---- launchers (kernels.cu); each returns cudaGetLastError() ----
 cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st);

@@ -24,8 +24,7 @@ cudaError_t launch_scan_0(const ScanParams& p, size_t smem, cudaStream_t st);
 // K2 dispatch by sub-vector length (template instantiations live in scan_s*.cu)
 cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st) {
   if (p.n_units <= 0) return cudaSuccess;
-  const int levels = (MTmax == 8) ? 7 : MTmax;
-  const size_t smem = (size_t)levels * 256 * 32 * 4 + 32 * 4 + 32 * 4 + 32 * 16 * 4 + 16;   // = scan_smem_bytes
+  const size_t smem = scan_smem(MTmax).total;
   const bool v4 = (p.luts == nullptr) && (p.d % 4 == 0) && p.vec4;
   switch (v4 ? p.s : 0) {
     case 16: return launch_scan_16(p, smem, st);

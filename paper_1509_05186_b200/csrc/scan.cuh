@@ -73,18 +73,23 @@ struct SmemScan {
   unsigned* thr;       // [32] CTA-shared top-k thresholds (float bits)
   int* qidx;           // [32] query of each lane
   float* stage;        // [32 queries][kDC dims] query sub-vector chunk (table build)
+  float* bigstage;     // 8-level trees: [8 levels][16 pairs][16 dims][2] staged queries
   uint32_t* tmem_slot; // TMEM base address written by tcgen05.alloc
   uint32_t tmem;       // TMEM base (level-0 tables of 8-level trees), 0 if unused
 };
 
 // ---------------------------------------------------------------------------
 // Tensor Memory (TMEM) as a lookup-table store.  An 8-level tree needs 8
-// tables of 32 KB for the CTA's 32 queries but shared memory holds 7; level 0
-// lives in TMEM: 256 columns x 32 lanes (lane = query), one copy per warp
-// quadrant (a warp may only address its own 32 TMEM lanes), read with
-// tcgen05.ld.32x32b.x1 by warp-uniform column = codeword.
+// tables of 32 KB for the CTA's 32 queries; levels 0 and 1 live in TMEM --
+// 2 x 256 columns x 32 lanes (lane = query, column = 256 * level + codeword),
+// one copy per warp quadrant (a warp may only address its own 32 TMEM lanes),
+// read with tcgen05.ld.32x32b.x1 at a warp-uniform column -- so shared memory
+// holds levels 2..7 plus a staging area for all 8 levels' query sub-vectors.
 // ---------------------------------------------------------------------------
-constexpr int kTmemCols = 256;
+constexpr int kTmemCols = 256 * kTmemLevels;
+
+// levels of a tree of MT levels held in TMEM
+__host__ __device__ constexpr int lv0_of(int MT) { return MT == 8 ? kTmemLevels : 0; }
 
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(slot);
@@ -115,13 +120,15 @@ __device__ __forceinline__ void tmem_wait_ld(uint32_t& x) {
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// Copy the level-0 table (global scratch row [256][32], just built by this CTA)
-// into each warp quadrant's TMEM lanes: warp w copies 64 columns for quadrant w&3.
+// Copy the TMEM levels (global scratch [kTmemLevels][256][32], just built by
+// this CTA) into each warp quadrant's TMEM lanes: warp w copies a quarter of
+// the columns for quadrant w & 3.
 __device__ void tmem_load_level0(const SmemScan& sm, const float* lut0) {
   const int lane = lane_id(), warp = warp_id();
-  const int sub = warp >> 2;               // 4 warps per quadrant
+  const int sub = warp >> 2;               // kWarps / 4 warps per quadrant
   const uint32_t tb = tmem_lane_base(sm.tmem);
-  for (int c0 = sub * 64; c0 < sub * 64 + 64; c0 += 8) {
+  constexpr int per = kTmemCols / (kWarps / 4);
+  for (int c0 = sub * per; c0 < sub * per + per; c0 += 8) {
     float v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = lut0[(c0 + j) * 32 + lane];
@@ -132,10 +139,11 @@ __device__ void tmem_load_level0(const SmemScan& sm, const float* lut0) {
 
 constexpr int kDC = 16;   // query dimensions staged per table-build pass
 
-// Table entry (level l, codeword k, query slot i): level 0 of an 8-level tree
-// lives in the global scratch row lut0 (7 levels fill shared memory).
+// Table entry (level l, codeword k, query slot i): the TMEM levels of an
+// 8-level tree are built into the global scratch lut0 [kTmemLevels][256][32]
+// and copied to TMEM (tmem_load_level0).
 __device__ __forceinline__ float* tab_slot(const SmemScan& sm, float* lut0, int l, int lv0, int k, int i) {
-  return (l < lv0) ? lut0 + k * 32 + i : sm.tab + tab_index(l - lv0, k, i);
+  return (l < lv0) ? lut0 + ((size_t)l * 256 + k) * 32 + i : sm.tab + tab_index(l - lv0, k, i);
 }
 
 // Inner loop of one build pass: codeword chunk c[0..NJ) (registers) against
@@ -211,18 +219,24 @@ __device__ __forceinline__ unsigned long long f2sqacc(unsigned long long t, unsi
   return r;
 }
 
-// Copy one table (smem region, swizzled [k][lane ^ (k & 31)]) into every warp
-// quadrant's TMEM lanes: warp w copies 64 columns for quadrant w & 3.
-__device__ __forceinline__ void tmem_load_from_smem(const SmemScan& sm, uint32_t region_s) {
+// Copy the two TMEM levels' tables (smem regions r0_s, r1_s, swizzled
+// [k][lane ^ (k & 31)]) into every warp quadrant's TMEM lanes: warp w copies
+// its share of the 512 columns for quadrant w & 3.
+__device__ __forceinline__ void tmem_load_from_smem(const SmemScan& sm, uint32_t r0_s, uint32_t r1_s) {
   const int lane = lane_id(), warp = warp_id();
   const int sub = warp >> 2;
   const uint32_t tb = tmem_lane_base(sm.tmem);
   const uint32_t lane4 = (uint32_t)lane << 2;
-  for (int c0 = sub * 64; c0 < sub * 64 + 64; c0 += 8) {
-    float v[8];
+  constexpr int per = kTmemCols / (kWarps / 4);
+  for (int c0 = sub * per; c0 < sub * per + per; c0 += 32) {   // 32 columns in flight per warp
+    const uint32_t rs = (c0 < 256) ? r0_s : r1_s;
+    float v[4][8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = lds(tab_addr(region_s, 0, (uint32_t)(c0 + j), lane4));
-    tmem_st8(tb + (uint32_t)c0, v);
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[g][j] = lds(tab_addr(rs, 0, (uint32_t)((c0 + 8 * g + j) & 255), lane4));
+#pragma unroll
+    for (int g = 0; g < 4; ++g) tmem_st8(tb + (uint32_t)(c0 + 8 * g), v[g]);
   }
   tmem_wait_st();
 }
@@ -242,40 +256,210 @@ template <int SS, int MT>
 __device__ __forceinline__ void stage_async(const ScanParams& p, int t, int chunk, int nch, uint32_t region_s,
                                             uint32_t stage_s) {
   const TreeDev& tr = p.tree[t];
-  const int i = threadIdx.x >> 4, j = threadIdx.x & (SS - 1);
-  int q = -1;
-  if (p.flatQ > 0) {
-    const int64_t s0 = (int64_t)chunk * p.flatQ / nch, s1 = (int64_t)(chunk + 1) * p.flatQ / nch;
-    q = (s0 + i < s1) ? (int)(s0 + i) : -1;
-  } else {
-    q = __ldg(p.chunk_q + (size_t)chunk * 32 + i);
-  }
-  if (q < 0) return;
-  const float* xr = p.queries + (size_t)q * p.d + j;
-  const uint32_t o = (uint32_t)(i >> 1) * 128u + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
+  const int j = threadIdx.x & (SS - 1);
 #pragma unroll
-  for (int l = 0; l < MT; ++l) {
-    const uint32_t dst = (l < MT - 1) ? region_s + (uint32_t)l * kStageLevelBytes + o : stage_s + o;
-    const float* src = xr + (size_t)p.lsub[tr.layer0 + l] * SS;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+  for (int i = threadIdx.x >> 4; i < 32; i += kThreads / SS) {   // query slot i, dimension j
+    int q = -1;
+    if (p.flatQ > 0) {
+      const int64_t s0 = (int64_t)chunk * p.flatQ / nch, s1 = (int64_t)(chunk + 1) * p.flatQ / nch;
+      q = (s0 + i < s1) ? (int)(s0 + i) : -1;
+    } else {
+      q = __ldg(p.chunk_q + (size_t)chunk * 32 + i);
+    }
+    if (q < 0) continue;
+    const float* xr = p.queries + (size_t)q * p.d + j;
+    const uint32_t o = (uint32_t)(i >> 1) * 128u + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
+#pragma unroll
+    for (int l = 0; l < MT; ++l) {
+      // 8 levels: every level in the staging area (region_s); else levels
+      // 0..MT-2 in the last level's region and MT-1 in the small stage
+      const uint32_t dst = (MT == 8 || l < MT - 1) ? region_s + (uint32_t)l * kStageLevelBytes + o : stage_s + o;
+      const float* src = xr + (size_t)p.lsub[tr.layer0 + l] * SS;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+    }
   }
 }
 
-// Resident-staging table build for s == 16 (every d = 128 configuration).
-// The active queries' sub-vectors are staged ONCE, as query pairs
+// Packed f32x2 subtract of a broadcast scalar: (a.lo - c, a.hi - c).  ptxas
+// encodes the duplicated 32-bit operand as FADD2's scalar form (R.F32).
+__device__ __forceinline__ unsigned long long f2subs(unsigned long long a, float c) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(((unsigned long long)__float_as_uint(c) << 32) | __float_as_uint(c)));
+  return r;
+}
+
+// Table build of an 8-level tree, s == 16 (every d = 128 configuration).
+// Levels 0 and 1 end up in TMEM, levels 2..7 in shared-memory regions 0..5;
+// the active queries' sub-vectors of all 8 levels are staged once, as query
+// pairs [level][pair][dim][2] in their own area (cp.async at kernel entry,
+// or synchronously with the coarse centroid subtracted for IVF residuals).
+// Four levels are built at a time by kWarps / 4 warps each; a warp owns
+// kR = 8 / (kWarps / 4) codeword rows per lane (rows kRow0 + 32 r + lane), so
+// every broadcast LDS.128 of a staged query pair (2 queries x 2 dims) feeds
+// 4 kR packed instructions (FADD2 with the codeword as the scalar operand,
+// then FFMA2) -- the shared-memory pipe stays well below the FP32 pipe.
+// Each entry is the j-ascending fp32 FMA chain sum_j (x_j - c_j)^2.
+// Round 0 builds levels 0..3 (levels 0 and 1 into regions 2 and 3, which
+// levels 4 and 5 only need in round 1; both are then copied to TMEM), round 1
+// levels 4..7.  Codewords of round 1 are loaded before the copy.
+constexpr int kWPL = kWarps / 4;          // warps per level
+constexpr int kR = 8 / kWPL;              // codeword rows per lane
+
+template <int SS>
+__device__ __forceinline__ void build_tables_resident8(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq,
+                                                       int cell, bool staged) {
+  static_assert(SS == kDC, "resident staging handles s == 16");
+  static_assert(kWPL * kR * 32 == 256, "four levels x 256 codewords per round");
+  const TreeDev& tr = p.tree[t];
+  const int K = p.K, d = p.d;
+  const int lane = lane_id(), warp = warp_id();
+  const uint32_t dsm_s = smem_u32(et_dsm);
+  const uint32_t tab_s = smem_u32(sm.tab);
+  const uint32_t stg_s = smem_u32(sm.bigstage);
+  const int np = (nq + 1) >> 1;                                          // query pairs
+  constexpr uint32_t pair_bytes = SS * 2 * 4;                            // 128 B per (level, pair)
+  if (staged) {
+    asm volatile("cp.async.wait_all;" ::: "memory");   // this thread's stage_async copies landed
+  } else {
+    __syncthreads();                                 // previous users of the tables / stage are done
+    const int j = threadIdx.x & (SS - 1);
+    for (int i = threadIdx.x >> 4; i < nq; i += kThreads / SS) {
+      float v[8];
+      const int q = sm.qidx[i];
+      const float* xr = p.queries + (size_t)q * d + j;
+      const float* cr = (cell >= 0 && p.coarse) ? p.coarse + (size_t)cell * d + j : nullptr;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) v[l] = __ldg(xr + (size_t)p.lsub[tr.layer0 + l] * SS);
+      if (cr) {
+#pragma unroll
+        for (int l = 0; l < 8; ++l) v[l] -= __ldg(cr + (size_t)p.lsub[tr.layer0 + l] * SS);
+      }
+      const uint32_t o = (uint32_t)(i >> 1) * pair_bytes + (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
+#pragma unroll
+      for (int l = 0; l < 8; ++l) sts(stg_s + (uint32_t)l * kStageLevelBytes + o, v[l]);
+    }
+  }
+  const int lw = warp / kWPL;                         // level within the round
+  const int row0 = (warp % kWPL) * 32 * kR;           // first codeword row of this warp
+  const bool active = row0 < K;                       // K < 256: idle codeword blocks
+  auto load_cw = [&](int l, float (&c)[kR][SS]) {
+    const int m = p.lsub[tr.layer0 + l];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int k = row0 + 32 * r + lane;
+      const float* row = p.codebooks + ((size_t)m * K + (k < K ? k : 0)) * SS;
+#pragma unroll
+      for (int j = 0; j < SS; j += 4) {
+        const float4 u = __ldg(reinterpret_cast<const float4*>(row + j));
+        c[r][j] = u.x; c[r][j + 1] = u.y; c[r][j + 2] = u.z; c[r][j + 3] = u.w;
+      }
+    }
+  };
+  // Entries of one table (region dst_s) for this lane's kR rows and every
+  // staged query pair of xs_s, two pairs per iteration.  Query slots >= nq and
+  // rows >= K are written but never looked up.
+  auto item = [&](uint32_t dst_s, uint32_t xs_s, const float (&c)[kR][SS]) {
+    const uint32_t rows = dst_s - dsm_s + ((uint32_t)(row0 + lane) << 7);   // row of r = 0 (byte offset)
+    const uint32_t sw = (uint32_t)(row0 + lane) << 2;   // swizzle (k & 31) << 2 -- the same for every r
+    uint32_t xo = xs_s - dsm_s;
+    uint32_t i4 = 0;                                 // 4 * (first query of the pair)
+    int pi = 0;
+    for (; pi + 1 < np; pi += 2, xo += 2 * pair_bytes, i4 += 16) {
+      unsigned long long a[2][kR];                   // (pair, row)
+#pragma unroll
+      for (int r = 0; r < kR; ++r) { a[0][r] = 0ull; a[1][r] = 0ull; }
+#pragma unroll
+      for (int j = 0; j < SS; j += 2) {
+        const float4 u0 = lds4_off(xo + (uint32_t)j * 8u), u1 = lds4_off(xo + pair_bytes + (uint32_t)j * 8u);
+        const unsigned long long p0 = f2pack(u0.x, u0.y), p1 = f2pack(u1.x, u1.y);
+        const unsigned long long q0 = f2pack(u0.z, u0.w), q1 = f2pack(u1.z, u1.w);
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          a[0][r] = f2sqacc(f2subs(p0, c[r][j]), a[0][r]);
+          a[1][r] = f2sqacc(f2subs(p1, c[r][j]), a[1][r]);
+        }
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          a[0][r] = f2sqacc(f2subs(q0, c[r][j + 1]), a[0][r]);
+          a[1][r] = f2sqacc(f2subs(q1, c[r][j + 1]), a[1][r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        float e0, o0, e1, o1;
+        f2unpack(a[0][r], e0, o0);
+        f2unpack(a[1][r], e1, o1);
+        const uint32_t row = rows + ((uint32_t)r << 12);   // row + 32 r
+        sts_off(row + ((i4 ^ sw) & 0x7cu), e0);
+        sts_off(row + (((i4 + 4) ^ sw) & 0x7cu), o0);
+        sts_off(row + (((i4 + 8) ^ sw) & 0x7cu), e1);
+        sts_off(row + (((i4 + 12) ^ sw) & 0x7cu), o1);
+      }
+    }
+    if (pi < np) {
+      unsigned long long a[kR];
+#pragma unroll
+      for (int r = 0; r < kR; ++r) a[r] = 0ull;
+#pragma unroll
+      for (int j = 0; j < SS; j += 2) {
+        const float4 u0 = lds4_off(xo + (uint32_t)j * 8u);
+        const unsigned long long p0 = f2pack(u0.x, u0.y), q0 = f2pack(u0.z, u0.w);
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          a[r] = f2sqacc(f2subs(p0, c[r][j]), a[r]);
+          a[r] = f2sqacc(f2subs(q0, c[r][j + 1]), a[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        float e0, o0;
+        f2unpack(a[r], e0, o0);
+        const uint32_t row = rows + ((uint32_t)r << 12);
+        sts_off(row + ((i4 ^ sw) & 0x7cu), e0);
+        sts_off(row + (((i4 + 4) ^ sw) & 0x7cu), o0);
+      }
+    }
+  };
+  float c[kR][SS];
+  if (active) load_cw(lw, c);
+  __syncthreads();                                   // stage complete
+  phase_mark(unit, 5);
+  // round 0: level lw -> region (levels 0, 1: regions 2, 3 until the TMEM copy)
+  const uint32_t r0 = (lw < 2) ? (uint32_t)(lw + 2) : (uint32_t)(lw - 2);
+  if (active) item(tab_s + (r0 << 15), stg_s + (uint32_t)lw * kStageLevelBytes, c);
+  if (active) load_cw(lw + 4, c);                    // round 1's rows, in flight during the copy
+  __syncthreads();
+  tmem_fence_after();
+  phase_mark(unit, 6);
+  tmem_load_from_smem(sm, tab_s + (2u << 15), tab_s + (3u << 15));
+  tmem_fence_before();
+  __syncthreads();                                   // regions 2, 3 free again
+  phase_mark(unit, 7);
+  // round 1: level lw + 4 -> region lw + 2
+  if (active) item(tab_s + ((uint32_t)(lw + 2) << 15), stg_s + (uint32_t)(lw + 4) * kStageLevelBytes, c);
+  __syncthreads();
+  tmem_fence_after();                                // TMEM levels visible to the scan's tcgen05.ld
+}
+
+// Resident-staging table build for s == 16 and trees of fewer than 8 levels
+// (8-level trees: build_tables_resident8).  The active queries' sub-vectors
+// are staged ONCE, as query pairs
 // [level][pair][dim][2], levels 0..MT-2 into the shared-memory region of the
 // tree's last level (built last) and level MT-1 into the small stage.  Warp w
 // owns codeword block kb = (w >> 1) & 7 (lane = codeword) and query-pair half
 // g = w & 1; for each level it keeps its codeword in registers and runs two
 // packed FADD2/FFMA2 chains (two query pairs, four entries) at a time against
-// broadcast LDS.128 loads of the staged pairs.  With 8 levels, level 0 is
-// built first into the region of level 6 and copied to TMEM.
+// broadcast LDS.128 loads of the staged pairs.
 template <int SS, int MT>
 __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const SmemScan& sm, int t, int unit,
                                                       int nq, int cell, bool staged) {
   static_assert(SS == kDC, "resident staging handles s == 16");
+  if constexpr (MT == 8) {
+    build_tables_resident8<SS>(p, sm, t, unit, nq, cell, staged);
+    return;
+  }
   const TreeDev& tr = p.tree[t];
-  constexpr int lv0 = (MT == 8) ? 1 : 0;   // level 0 of an 8-level tree lives in TMEM
+  constexpr int lv0 = 0;
   const int K = p.K, d = p.d;
   const int lane = lane_id(), warp = warp_id();
   const uint32_t tab_s = smem_u32(sm.tab);
@@ -288,8 +472,8 @@ __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const
   } else {
     __syncthreads();                                 // previous tree's scan is done with the tables
     // thread -> (query slot i, dim j); all loads first, then the stores
-    const int i = threadIdx.x >> 4, j = threadIdx.x & (SS - 1);
-    if (i < nq) {
+    const int j = threadIdx.x & (SS - 1);
+    for (int i = threadIdx.x >> 4; i < nq; i += kThreads / SS) {
       float v[MT];
       const int q = sm.qidx[i];
       const float* xr = p.queries + (size_t)q * d + j;
@@ -306,10 +490,11 @@ __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const
       sts(stage_s + o, v[MT - 1]);
     }
   }
-  const int kb = (warp >> 1) & 7, g = warp & 1;
+  constexpr int WG = kWarps / 8;                     // warps per codeword block (query-pair groups)
+  const int kb = (warp / WG) & 7, g = warp % WG;
   const int k = kb * 32 + lane;
   const bool kvalid = k < K;
-  const int p0 = g ? (np + 1) >> 1 : 0, p1 = g ? np : (np + 1) >> 1;
+  const int p0 = g ? (np + 1) >> 1 : 0, p1 = (g || WG == 1) ? np : (np + 1) >> 1;
   const bool active = kb * 32 < K;                   // K < 256: idle codeword blocks
   const uint32_t dsm_s = smem_u32(et_dsm);
   auto load_cw = [&](int l, float (&c)[SS]) {
@@ -368,26 +553,8 @@ __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const
   if (active) load_cw(0, cw);
   __syncthreads();                                   // stage complete
   phase_mark(unit, 5);
-  if constexpr (MT == 8) {
-    // level 0 -> region of level 6 (free until level 6 is built) -> TMEM
-    const uint32_t l0_s = tab_s + (5u << 15);
-    if (active) {
-      load_cw(1, cwn);
-      item(l0_s, region_s, cw);
-#pragma unroll
-      for (int j = 0; j < SS; ++j) cw[j] = cwn[j];
-    }
-    __syncthreads();
-    tmem_fence_after();
-    tmem_load_from_smem(sm, l0_s);   // overlaps the other warps' level-1.. builds
-    tmem_fence_before();
-    phase_mark(unit, 6);
-  }
   // levels lv0 .. MT-2 (their queries staged in the last level's region)
   for (int l = lv0; l < MT - 1; ++l) {
-    // level 6 of an 8-level tree reuses level 0's staging region: every warp's
-    // TMEM copy must be done
-    if (MT == 8 && l == MT - 2) __syncthreads();
     if (active) {
       load_cw(l + 1, cwn);                           // prefetch the next level's codeword
       item(tab_s + ((uint32_t)(l - lv0) << 15), region_s + (uint32_t)l * kStageLevelBytes, cw);
@@ -399,7 +566,6 @@ __device__ __forceinline__ void build_tables_resident(const ScanParams& p, const
   phase_mark(unit, 7);
   if (active) item(region_s, stage_s, cw);
   __syncthreads();
-  if constexpr (MT == 8) tmem_fence_after();         // TMEM level 0 visible to the scan's tcgen05.ld
 }
 
 // Few queries with long sub-vectors (c3: s = 60, <= 8 queries per CTA): one
@@ -414,31 +580,42 @@ __device__ void build_tables_wide(const ScanParams& p, const SmemScan& sm, int t
   constexpr int NCH = (SS + kDC - 1) / kDC;
   const TreeDev& tr = p.tree[t];
   const int MT = tr.MT;
-  const int lv0 = (MT == 8) ? 1 : 0;
+  const int lv0 = lv0_of(MT);
   const int K = p.K, d = p.d;
   const int lane = lane_id(), warp = warp_id();
-  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
+  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * kTmemLevels * 256 * 32 : nullptr;
+  constexpr int WG = kWarps / 8;                // query groups (warps per codeword block)
+  constexpr int NQW = 8 / WG;                   // query slots per warp: g, g + WG, ...
+  constexpr int SPT = 512 / kThreads;           // staging elements (8 x 64) per thread
   const int kb = warp & 7, g = warp >> 3;
   const int k = kb * 32 + lane;
   const bool kvalid = k < K;
-  const int si = threadIdx.x >> 6, sj = threadIdx.x & 63;   // staging element (8 x 64)
-  const int sq = (si < nq) ? sm.qidx[si] : -1;
-  auto fetch = [&](int l) -> float {
+  auto fetch = [&](int l, int e) -> float {     // staging element e = (slot e >> 6, dim e & 63)
+    const int si = e >> 6, sj = e & 63;
+    const int sq = (si < nq) ? sm.qidx[si] : -1;
     if (sq < 0 || sj >= SS) return 0.f;
     const int m = p.lsub[tr.layer0 + l];
     float v = __ldg(p.queries + (size_t)sq * d + (size_t)m * SS + sj);
     if (cell >= 0 && p.coarse) v -= __ldg(p.coarse + (size_t)cell * d + (size_t)m * SS + sj);
     return v;
   };
-  float nxt = fetch(0);
+  float nxt[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) nxt[u] = fetch(0, threadIdx.x + u * kThreads);
   __syncthreads();                              // previous users of the stage are done
-  sm.stage[threadIdx.x] = nxt;
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) sm.stage[threadIdx.x + u * kThreads] = nxt[u];
   __syncthreads();
   for (int l = 0; l < MT; ++l) {
-    if (l + 1 < MT) nxt = fetch(l + 1);         // next level's stage value
+    if (l + 1 < MT) {                           // next level's stage values
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) nxt[u] = fetch(l + 1, threadIdx.x + u * kThreads);
+    }
     const int m = p.lsub[tr.layer0 + l];
     const float* crow = p.codebooks + ((size_t)m * K + (kvalid ? k : 0)) * SS;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float acc[NQW];
+#pragma unroll
+    for (int qq = 0; qq < NQW; ++qq) acc[qq] = 0.f;
     float c[kDC], cn[kDC];
 #pragma unroll
     for (int j = 0; j < kDC; j += 4) {
@@ -457,8 +634,8 @@ __device__ void build_tables_wide(const ScanParams& p, const SmemScan& sm, int t
       }
       constexpr int NJ0 = SS - (NCH - 1) * kDC;   // size of the last chunk
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const int i = g + 2 * qq;
+      for (int qq = 0; qq < NQW; ++qq) {
+        const int i = g + WG * qq;
         if (i < nq) {
           const float* x = sm.stage + i * 64 + jc * kDC;
 #pragma unroll
@@ -474,12 +651,15 @@ __device__ void build_tables_wide(const ScanParams& p, const SmemScan& sm, int t
       for (int j = 0; j < kDC; ++j) c[j] = cn[j];
     }
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq) {
-      const int i = g + 2 * qq;
+    for (int qq = 0; qq < NQW; ++qq) {
+      const int i = g + WG * qq;
       if (i < nq && kvalid) *tab_slot(sm, lut0, l, lv0, k, i) = acc[qq];
     }
     __syncthreads();
-    if (l + 1 < MT) sm.stage[threadIdx.x] = nxt;
+    if (l + 1 < MT) {
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) sm.stage[threadIdx.x + u * kThreads] = nxt[u];
+    }
     __syncthreads();
   }
 }
@@ -496,12 +676,12 @@ template <int SS, int DC = kDC>
 __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int unit, int nq, int cell) {
   const TreeDev& tr = p.tree[t];
   const int MT = tr.MT;
-  const int lv0 = (MT == 8) ? 1 : 0;
+  const int lv0 = lv0_of(MT);
   const int K = p.K, d = p.d;
   const int s = (SS > 0) ? SS : p.s;
   const int nb = (K + 31) >> 5;
   const int lane = lane_id(), warp = warp_id();
-  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
+  float* lut0 = p.lut0 ? p.lut0 + (size_t)unit * kTmemLevels * 256 * 32 : nullptr;
   if (p.luts) {   // materialised tables: copy
     for (int item = warp; item < MT * nb; item += kWarps) {
       const int l = item / nb, kb = item - l * nb;
@@ -519,10 +699,12 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
   const int G = max(1, kWarps / nb);            // query groups
   const int kb = warp % nb, g = warp / nb;
   const bool computes = g < G;
-  // staging element of this thread: query slot si, dimension sj of the chunk
-  const int si = threadIdx.x / DC, sj = threadIdx.x % DC;
-  const int sq = (si < nq) ? sm.qidx[si] : -1;
-  auto fetch = [&](int pass) -> float {
+  // staging elements of this thread: e = threadIdx.x + u * kThreads -> query
+  // slot e / DC, dimension e % DC of the chunk
+  constexpr int SPG = (32 * DC + kThreads - 1) / kThreads;
+  auto fetch = [&](int pass, int e) -> float {
+    const int si = e / DC, sj = e % DC;
+    const int sq = (si < nq && si < 32) ? sm.qidx[si] : -1;
     const int l = pass / npl, jc = pass - l * npl;
     const int j = jc * DC + sj;
     if (sq < 0 || j >= s) return 0.f;
@@ -556,13 +738,18 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
   constexpr bool kPrefetchCw = (DC == kDC);
   float cw[DC], cwn[kPrefetchCw ? DC : 1];
   fetch_cw(0, cw);
-  float nxt = fetch(0);
+  float nxt[SPG];
+#pragma unroll
+  for (int u = 0; u < SPG; ++u) nxt[u] = fetch(0, threadIdx.x + u * kThreads);
   __syncthreads();                              // previous users of the stage are done
-  if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
+#pragma unroll
+  for (int u = 0; u < SPG; ++u)
+    if (threadIdx.x + u * kThreads < 32 * kDC) sm.stage[threadIdx.x + u * kThreads] = nxt[u];
   __syncthreads();
   for (int pass = 0; pass < P; ++pass) {
     if (pass + 1 < P) {                         // prefetch the next pass: stage values (+ codeword chunk)
-      nxt = fetch(pass + 1);
+#pragma unroll
+      for (int u = 0; u < SPG; ++u) nxt[u] = fetch(pass + 1, threadIdx.x + u * kThreads);
       if constexpr (kPrefetchCw) fetch_cw(pass + 1, cwn);
     }
     const int l = pass / npl, jc = pass - l * npl;
@@ -579,7 +766,9 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
     }
     __syncthreads();
     if (pass + 1 < P) {
-      if (threadIdx.x < 32 * kDC) sm.stage[threadIdx.x] = nxt;
+#pragma unroll
+      for (int u = 0; u < SPG; ++u)
+        if (threadIdx.x + u * kThreads < 32 * kDC) sm.stage[threadIdx.x + u * kThreads] = nxt[u];
       if constexpr (kPrefetchCw) {
 #pragma unroll
         for (int j = 0; j < DC; ++j) cw[j] = cwn[j];
@@ -596,7 +785,7 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
 // (distance, id) pairs: t = smallest distance whose cumulative multiplicity
 // reaches k; all candidates < t; of the candidates == t, those whose smallest
 // id ranks below k - (multiplicity < t).  Returns the new count and threshold.
-constexpr int kRefreshPer = (2 * kTopkMax + 96) / 32;   // entries per lane held in registers
+constexpr int kRefreshPer = (2 * kTopkMax + kBatchEmit) / 32;   // entries per lane held in registers (>= B)
 
 __device__ __noinline__ void refresh_buffer(uint2* buf, int n, int k, const uint32_t* gmult,
                                             const int32_t* gminid, int* new_cnt, float* new_thr) {
@@ -677,6 +866,7 @@ __device__ __noinline__ void refresh_buffer(uint2* buf, int n, int k, const uint
 struct TopkState {
   float thr;
   int cnt;
+  uint32_t msum;      // sum of 2^bucket (<= multiplicity) of the candidates emitted so far
   uint2* buf;         // this lane's buffer
   uint2* warp_buf;    // lane 0's buffer of this warp (lane L's = warp_buf + L*kWarps*B)
   bool active;
@@ -694,8 +884,8 @@ struct EmitCtx {
 
 // Append one group's distance to this lane's candidates if it can still be in
 // the top-k (hot path: no calls, no syncs).  Buffers are pruned at batch
-// boundaries by maybe_refresh, which keeps >= 64 free slots per lane (a batch
-// of 32 leaves of each of a warp's two streams).
+// boundaries by maybe_refresh, which keeps >= kBatchEmit free slots per lane
+// (a batch of 32 leaves of each of a warp's kStreams streams).
 __device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, uint32_t mult) {
   const ScanParams& p = *e.p;
   if (p.mode == kModeFull) {
@@ -718,13 +908,13 @@ struct CntThr { int cnt; float thr; };
 // 0x7f7f7f7f (~3.4e38) by a memset; kThrNone marks "no bound yet".
 constexpr float kThrNone = 1e38f;
 
-__device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr, int B, int k,
+__device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr, uint32_t msum, int B, int k,
                                              const uint32_t* gmult, const int32_t* gminid) {
   const int lane = lane_id();
   // full buffers, and (once) buffers that first reach k candidates while the
   // lane has no threshold yet: an early exact bound stops the flood of
   // candidates that every fresh warp would otherwise emit
-  unsigned full = __ballot_sync(FULLMASK, cnt > B - 64 || (cnt >= k && !(thr < kThrNone)));
+  unsigned full = __ballot_sync(FULLMASK, cnt > B - kBatchEmit || ((cnt >= k || msum >= (uint32_t)k) && !(thr < kThrNone)));
   while (full) {
     const int L = __ffs(full) - 1;
     full &= full - 1;
@@ -738,8 +928,9 @@ __device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr
 
 __device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
   const ScanParams& p = *e.p;
-  if (__any_sync(FULLMASK, e.ts.cnt > p.B - 64 || (e.ts.cnt >= p.k && !(e.ts.thr < kThrNone)))) {
-    const CntThr r = maybe_refresh(e.ts.warp_buf, e.ts.cnt, e.ts.thr, p.B, p.k, p.group_mult, p.group_minid);
+  if (__any_sync(FULLMASK, e.ts.cnt > p.B - kBatchEmit ||
+                             ((e.ts.cnt >= p.k || e.ts.msum >= (uint32_t)p.k) && !(e.ts.thr < kThrNone)))) {
+    const CntThr r = maybe_refresh(e.ts.warp_buf, e.ts.cnt, e.ts.thr, e.ts.msum, p.B, p.k, p.group_mult, p.group_minid);
     e.ts.cnt = r.cnt;
     e.ts.thr = r.thr;
   }
@@ -749,10 +940,11 @@ __device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
 // pre-swizzled byte offset of table entry (level l, k = code byte l) inside
 // that level's 32 KB shared-memory region, (k << 7) | ((k & 31) << 2), so a
 // lookup is one extract/XOR with the lane's offset and one LDS whose immediate
-// carries the level's region base.  Level 0 of an 8-level tree lives in TMEM:
-// its half-word is the column k (bits 0..7) with the LCP with the previous
-// leaf in bits 8..11 and floor(log2(multiplicity)) in bits 12..15; trees with
-// MT < 8 keep both in half-word 7 (bits 0..3, 4..7).
+// carries the level's region base.  Levels 0 and 1 of an 8-level tree live in
+// TMEM: their half-words are the columns k0, k1 (bits 0..7); half-word 0
+// carries the LCP with the previous leaf in bits 8..11 and
+// floor(log2(multiplicity)) in bits 12..15; trees with MT < 8 keep both in
+// half-word 7 (bits 0..3, 4..7).
 
 // The scan kernel has no static shared memory, so its dynamic shared memory
 // (the tables, at offset 0) starts at the fixed shared-window address
@@ -785,29 +977,89 @@ __device__ __forceinline__ uint32_t rec_mbucket(const uint4& r) {
 template <int MT>
 __device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t pl, bool valid,
                                          uint32_t lane4, uint32_t tq) {
-  constexpr int lv0 = (MT == 8) ? 1 : 0;
+  constexpr int lv0 = lv0_of(MT);
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
   const uint32_t plv = valid ? pl : 255u;   // 255: no level is looked up
-  if constexpr (lv0 == 1) {
-    // level 0 (TMEM) only on a new first-level subtree: a warp-uniform predicate
-    uint32_t t0 = __float_as_uint(v[0]);
+  if constexpr (lv0 == 2) {
+    // levels 0 and 1 (TMEM, columns k0 and 256 + k1) only on a new subtree at
+    // depth 0 / <= 1: warp-uniform predicates
+    uint32_t t0 = __float_as_uint(v[0]), t1 = __float_as_uint(v[1]);
     asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.u32 q, %2, 0;\n\t"
                  "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
                  : "+r"(t0) : "r"(tq + (w[0] & 255u)), "r"(plv));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0));
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.le.u32 q, %2, 1;\n\t"
+                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
+                 : "+r"(t1) : "r"(tq + 256u + ((w[0] >> 16) & 255u)), "r"(plv));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0), "+r"(t1));
     v[0] = __uint_as_float(t0);
+    v[1] = __uint_as_float(t1);
   }
 #pragma unroll
   for (int l = lv0; l < MT; ++l) {
     const uint32_t off = (l & 1) ? ((w[l >> 1] >> 16) ^ lane4) : ((w[l >> 1] & 0xffffu) ^ lane4);
-    const uint32_t addr = off + (kDsmBase + ((uint32_t)(l - lv0) << 15));
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.le.u32 q, %2, %3;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
-                 : "+f"(v[l]) : "r"(addr), "r"(plv), "r"((uint32_t)l));
+    // predicated LDS (the compiler's predicate: no shared-memory access when off)
+    if (plv <= (uint32_t)l) v[l] = *reinterpret_cast<const float*>(et_dsm + off + ((uint32_t)(l - lv0) << 15));
   }
   float s = v[0];
 #pragma unroll
   for (int l = 1; l < MT; ++l) s = s + v[l];
   return s;
+}
+
+// ---- masked records: fused E-Forest tuples ----
+// Tuple t's record is the single-tree record of its full code with the LCP
+// field replaced by an 8-bit lookup mask: bit l is set iff level l's entry
+// must be (re)looked up, i.e. l - split[u] >= the LCP of tuples t-1 and t over
+// the bytes of the tree u that holds level l -- each tree's own Distance
+// Context carried along the tuple sequence.  M == 8: mask in
+// half-word 0 bits 8..15 (next to the TMEM column k0), multiplicity bucket
+// in half-word 1 bits 8..11 (next to the TMEM column k1); M < 8: half-word 7
+// = mask | bucket << 8.
+template <int MT>
+__device__ __forceinline__ uint32_t rec_mask(const uint4& r) {
+  if constexpr (MT == 8) return (r.x >> 8) & 255u;
+  else return (r.w >> 16) & 255u;
+}
+template <int MT>
+__device__ __forceinline__ uint32_t rec_mbucket_m(const uint4& r) {
+  if constexpr (MT == 8) return (r.x >> 24) & 15u;
+  else return (r.w >> 24) & 15u;
+}
+
+// dc_leaf for masked records: level l is looked up iff bit l of `mask`
+// (warp-uniform); the distance is summed per forest tree left to right and
+// the per-tree partials in tree order, ((p_0 + p_1) + ...) (reading A13):
+// bit l of `fsplit` marks the first level of tree u >= 1.
+template <int MT>
+__device__ __forceinline__ float dc_leaf_m(float (&v)[MT], const uint4& r, uint32_t mask, uint32_t lane4,
+                                           uint32_t tq, uint32_t fsplit) {
+  constexpr int lv0 = lv0_of(MT);
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  if constexpr (lv0 == 2) {
+    uint32_t t0 = __float_as_uint(v[0]), t1 = __float_as_uint(v[1]);
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
+                 : "+r"(t0) : "r"(tq + (w[0] & 255u)), "r"(mask & 1u));
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
+                 : "+r"(t1) : "r"(tq + 256u + ((w[0] >> 16) & 255u)), "r"(mask & 2u));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0), "+r"(t1));
+    v[0] = __uint_as_float(t0);
+    v[1] = __uint_as_float(t1);
+  }
+#pragma unroll
+  for (int l = lv0; l < MT; ++l) {
+    const uint32_t off = (((l & 1) ? (w[l >> 1] >> 16) : w[l >> 1]) & 0x7ffcu) ^ lane4;
+    if (mask & (1u << l)) v[l] = *reinterpret_cast<const float*>(et_dsm + off + ((uint32_t)(l - lv0) << 15));
+  }
+  float tot = 0.f, s = v[0];
+  bool have = false;
+#pragma unroll
+  for (int l = 1; l < MT; ++l) {
+    if ((fsplit >> l) & 1u) { tot = have ? tot + s : s; have = true; s = v[l]; }
+    else s = s + v[l];
+  }
+  return have ? tot + s : s;
 }
 
 // Scan of leaves [a, b) of one tree by one warp, lane = query.  The range is
@@ -889,6 +1141,124 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
       }
       batch_end();
     }
+  }
+}
+
+// Top-k / full-output scan of leaves [a, b) of one tree (or of the fused
+// forest's tuples) by one warp, lane = query.  The range is split into NS
+// contiguous streams scanned in lockstep -- NS independent dependency chains
+// per warp, one branch-free block per step (lengths differ by at most one
+// leaf: the shorter streams' last step is predicated off).  Records come with
+// one coalesced load per 32 leaves per stream (the next batch in flight) and
+// four shuffles per leaf; a leaf costs (MT - LCP) shared-memory / TMEM
+// lookups (masked records: the levels of its mask), MT - 1 FADDs and a
+// predicated emit.
+template <int MT, bool MASKED, bool TOPK, int NS>
+__device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b) {
+  const ScanParams& p = *e.p;
+  const int lane = lane_id();
+  const uint32_t lane4 = (uint32_t)lane << 2;
+  const uint32_t tq = tmem_lane_base(sm.tmem);
+  const uint4* rec = tr.rec;
+  constexpr uint32_t kAll = (1u << MT) - 1u;
+  auto shfl_rec = [&](const uint4& mine, int j) {
+    uint4 r;
+    r.x = __shfl_sync(FULLMASK, mine.x, j);
+    r.y = (MT > 2 || MASKED) ? __shfl_sync(FULLMASK, mine.y, j) : 0u;
+    r.z = (MT > 4) ? __shfl_sync(FULLMASK, mine.z, j) : 0u;
+    r.w = __shfl_sync(FULLMASK, mine.w, j);
+    return r;
+  };
+  const uint32_t len = b - a;
+  uint32_t s0[NS], sl[NS];                           // stream start, length
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    s0[k] = a + (uint32_t)(((uint64_t)len * k) / NS);
+    sl[k] = a + (uint32_t)(((uint64_t)len * (k + 1)) / NS) - s0[k];
+  }
+  uint32_t steps = 0;                                // the longest stream (lengths differ by <= 1)
+#pragma unroll
+  for (int k = 0; k < NS; ++k) steps = max(steps, sl[k]);
+  auto load_batch = [&](int k, uint32_t off) {
+    return (off + lane < sl[k]) ? __ldg(rec + s0[k] + off + lane) : make_uint4(0u, 0u, 0u, 0u);
+  };
+  uint4 nx[NS];
+  float v[NS][MT];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    nx[k] = load_batch(k, 0);
+#pragma unroll
+    for (int l = 0; l < MT; ++l) v[k][l] = 0.f;
+  }
+  for (uint32_t off = 0; off < steps; off += 32) {
+    uint4 cur[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      cur[k] = nx[k];
+      nx[k] = load_batch(k, off + 32);
+    }
+    const int n = (int)min(32u, steps - off);
+    for (int j = 0; j < n; ++j) {
+      const bool first = (off + j == 0);             // range start: rebuild the path
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const bool ok = off + j < sl[k];
+        const uint4 r = shfl_rec(cur[k], j);
+        float dist;
+        if constexpr (MASKED) {
+          dist = dc_leaf_m<MT>(v[k], r, ok ? (first ? kAll : rec_mask<MT>(r)) : 0u, lane4, tq, p.fsplit);
+        } else {
+          dist = dc_leaf<MT>(v[k], r, first ? 0u : rec_lcp<MT>(r), ok, lane4, tq);
+        }
+        const uint32_t lf = s0[k] + off + j;
+        if constexpr (!TOPK) {
+          if (ok) p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + lf] = dist;   // query-major rows
+        } else {
+          TopkState& ts = e.ts;
+          const uint32_t bucket = MASKED ? rec_mbucket_m<MT>(r) : rec_mbucket<MT>(r);
+          const bool em = ok && ts.active && dist <= ts.thr;
+          if (em) ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), lf);
+          ts.cnt += em ? 1 : 0;
+          ts.msum += em ? (1u << bucket) : 0u;
+          // one group alone (2^bucket <= multiplicity ids) bounds the k-th distance
+          if (em && (1u << bucket) >= (uint32_t)p.k) ts.thr = dist;
+        }
+      }
+    }
+    if constexpr (TOPK) {   // prune full buffers; share the threshold with the CTA's other warps
+      refresh_if_needed(e);  // and with every other unit scanning the same query
+      if (e.ts.active) {
+        const unsigned mine = __float_as_uint(e.ts.thr);
+        atomicMin(&sm.thr[lane], mine);
+        unsigned t = *((volatile unsigned*)&sm.thr[lane]);
+        if (p.qthr_shared) t = min(t, atomicMin(p.qthr + e.q, t));
+        e.ts.thr = __uint_as_float(t);
+      }
+    }
+  }
+}
+
+
+template <int MT, bool MASKED>
+__device__ __forceinline__ void scan_tree3_mode(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a,
+                                                uint32_t b) {
+  if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, kStreams>(e, sm, tr, a, b);
+  else scan_tree3<MT, MASKED, false, kStreams>(e, sm, tr, a, b);
+}
+
+template <bool MASKED>
+__device__ __forceinline__ void scan2_dispatch(EmitCtx& e, const SmemScan& sm, const TreeDev& tr,
+                                               uint32_t a, uint32_t b) {
+  switch (tr.MT) {
+    case 1: scan_tree3_mode<1, MASKED>(e, sm, tr, a, b); break;
+    case 2: scan_tree3_mode<2, MASKED>(e, sm, tr, a, b); break;
+    case 3: scan_tree3_mode<3, MASKED>(e, sm, tr, a, b); break;
+    case 4: scan_tree3_mode<4, MASKED>(e, sm, tr, a, b); break;
+    case 5: scan_tree3_mode<5, MASKED>(e, sm, tr, a, b); break;
+    case 6: scan_tree3_mode<6, MASKED>(e, sm, tr, a, b); break;
+    case 7: scan_tree3_mode<7, MASKED>(e, sm, tr, a, b); break;
+    case 8: scan_tree3_mode<8, MASKED>(e, sm, tr, a, b); break;
+    default: break;
   }
 }
 
@@ -980,8 +1350,12 @@ __device__ __forceinline__ void scan_any(EmitCtx& e, const SmemScan& sm, const T
 }
 
 
-template <int SS, int MTC, bool FOREST>
+// MODE 0: one E-Tree (or IVF lists); 1: E-Forest with per-tree partials and
+// the tuple join (M > 8, e.g. c3); 2: fused E-Forest over masked tuple
+// records (M <= 8, e.g. c5).
+template <int SS, int MTC, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant__ ScanParams p) {
+  constexpr bool FOREST = (MODE == 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int unit = blockIdx.x;
   const int chunk = unit / p.S;
@@ -992,27 +1366,26 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   if (p.n_chunks_dev && chunk >= *p.n_chunks_dev) return;   // IVF: fewer chunks than the bound
   int MTmax = 0;
   for (int t = 0; t < p.T; ++t) MTmax = max(MTmax, p.tree[t].MT);
-  const int smem_levels = (MTmax == 8) ? 7 : MTmax;
+  const ScanSmem L = scan_smem(MTmax);
   // resident build of the first tree: stage the queries asynchronously now
   constexpr bool kResident = (SS == kDC && MTC > 0);
   const bool staged = kResident && !p.luts && !p.chunk_cell;
   if constexpr (kResident) {
     if (staged) {
       const int MTf = p.tree[p.T - 1].MT;
-      const size_t reg = (size_t)smem_levels * 256 * 32 * 4;
       const uint32_t base = smem_u32(smem_raw);
-      const uint32_t region_s = base + ((uint32_t)(MTf - 1 - (MTf == 8 ? 1 : 0)) << 15);
-      const uint32_t stage_s = base + (uint32_t)reg + 32u * 4u + 32u * 4u;   // = sm.stage below
-      stage_async<SS, MTC>(p, p.T - 1, chunk, p.n_units / p.S, region_s, stage_s);
+      // 8 levels: the staging area; else the last level's region + the small stage
+      const uint32_t region_s = (MTf == 8) ? base + L.big_stage : base + ((uint32_t)(MTf - 1) << 15);
+      stage_async<SS, MTC>(p, p.T - 1, chunk, p.n_units / p.S, region_s, base + L.stage);
     }
   }
   SmemScan sm;
   sm.tab = reinterpret_cast<float*>(smem_raw);
-  const size_t region = (size_t)smem_levels * 256 * 32 * 4;
-  sm.thr = reinterpret_cast<unsigned*>(smem_raw + region);
-  sm.qidx = reinterpret_cast<int*>(sm.thr + 32);
-  sm.stage = reinterpret_cast<float*>(sm.qidx + 32);
-  sm.tmem_slot = reinterpret_cast<uint32_t*>(sm.stage + 32 * kDC);
+  sm.bigstage = reinterpret_cast<float*>(smem_raw + L.big_stage);
+  sm.thr = reinterpret_cast<unsigned*>(smem_raw + L.thr);
+  sm.qidx = reinterpret_cast<int*>(smem_raw + L.qidx);
+  sm.stage = reinterpret_cast<float*>(smem_raw + L.stage);
+  sm.tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + L.tmem_slot);
   sm.tmem = 0;
   const bool use_tmem = (MTmax == 8);
   if (use_tmem) {
@@ -1041,7 +1414,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     nq = __popc(__ballot_sync(FULLMASK, q >= 0));   // active lanes are a prefix
   }
   const int cell = p.chunk_cell ? __ldg(p.chunk_cell + chunk) : -1;
-  const float* lut0g = p.lut0 ? p.lut0 + (size_t)unit * 256 * 32 : nullptr;
+  const float* lut0g = p.lut0 ? p.lut0 + (size_t)unit * kTmemLevels * 256 * 32 : nullptr;
 
   EmitCtx e;
   e.p = &p;
@@ -1052,6 +1425,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   e.ts.active = lane < nq;
   e.ts.thr = e.ts.active ? __int_as_float(0x7f800000) : -1.0f;
   e.ts.cnt = 0;
+  e.ts.msum = 0;
   e.ts.warp_buf = nullptr;
   e.ts.buf = nullptr;
   if (p.mode == kModeTopk) {
@@ -1104,8 +1478,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     if (wa < wb) {
       if constexpr (FOREST) {
         scan_any<MTC, 0>(e, sm, tr, wa, wb, lut0g);   // per-leaf partials of every tree
+      } else if constexpr (MTC > 0) {
+        scan_tree3_mode<MTC, MODE == 2>(e, sm, tr, wa, wb);
       } else {
-        scan_any<MTC, 1>(e, sm, tr, wa, wb, lut0g);
+        scan2_dispatch<MODE == 2>(e, sm, tr, wa, wb);
       }
     }
     tmem_fence_before();
@@ -1211,18 +1587,13 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   phase_mark(unit, 4);
 }
 
-inline size_t scan_smem_bytes(int MTmax) {
-  const int levels = (MTmax == 8) ? 7 : MTmax;
-  const size_t tab = (size_t)levels * 256 * 32 * 4;
-  return tab + 32 * 4 + 32 * 4 + 32 * kDC * 4 + 16;
-}
 
-template <int SS, int MTC, bool FOREST>
+template <int SS, int MTC, int MODE>
 static cudaError_t launch_scan_t(const ScanParams& p, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS, MTC, FOREST>,
+  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS, MTC, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  scan_kernel<SS, MTC, FOREST><<<p.n_units, kThreads, smem, st>>>(p);
+  scan_kernel<SS, MTC, MODE><<<p.n_units, kThreads, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -1232,10 +1603,21 @@ cudaError_t launch_scan_s(const ScanParams& p, size_t smem, cudaStream_t st) {
   bool uni = true;
   for (int t = 1; t < p.T; ++t) uni = uni && (p.tree[t].MT == p.tree[0].MT);
   const int mt = uni ? p.tree[0].MT : 0;
-  const bool forest = p.T > 1;
-  if (mt == 8) return forest ? launch_scan_t<SS, 8, true>(p, smem, st) : launch_scan_t<SS, 8, false>(p, smem, st);
-  if (mt == 4) return forest ? launch_scan_t<SS, 4, true>(p, smem, st) : launch_scan_t<SS, 4, false>(p, smem, st);
-  return forest ? launch_scan_t<SS, 0, true>(p, smem, st) : launch_scan_t<SS, 0, false>(p, smem, st);
+  if (p.T > 1) {   // per-tree partials + join
+    if constexpr (SS != 16) {   // (s = 16 forests have M <= 8 levels of 16 dims: fused)
+      if (mt == 8) return launch_scan_t<SS, 8, 1>(p, smem, st);
+    }
+    return launch_scan_t<SS, 0, 1>(p, smem, st);
+  }
+  if (p.masked) {  // fused forest
+    if constexpr (SS != 60) {
+      if (mt == 8) return launch_scan_t<SS, 8, 2>(p, smem, st);
+    }
+    return launch_scan_t<SS, 0, 2>(p, smem, st);
+  }
+  if (mt == 8) return launch_scan_t<SS, 8, 0>(p, smem, st);
+  if (mt == 4) return launch_scan_t<SS, 4, 0>(p, smem, st);
+  return launch_scan_t<SS, 0, 0>(p, smem, st);
 }
 
 }  // namespace

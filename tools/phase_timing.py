@@ -1,7 +1,7 @@
 """Per-CTA phase durations of the scan kernel (experiment build with -DET_PHASE_TIMING).
 
   python tools/phase_timing.py --config c2
-Phases: 0 start, 1 build start, 5 staged, 6 level 0 in TMEM, 7 levels 1..MT-2 built,
+Phases: 0 start, 1 build start, 5 staged, 6 round 0 built (levels 0-3), 7 TMEM levels copied,
 2 build done, 3 scan done, 4 compaction done.
 """
 import argparse
@@ -25,10 +25,13 @@ def main():
     a = ap.parse_args()
     import torch
     from paper_1509_05186_b200 import api
-    cfg = bench.workload_config(a.config)
+    from paper_1509_05186_b200 import synth
+    cfg = synth.CONFIGS[a.config]
     dev = torch.device("cuda", 0)
-    st = bench.prepare_ours(cfg, dev, 0, 1)
-    ix = st["ix"]
+    st = bench.prepare(cfg, {}, bench.CudaBackend(dev), bench.Comm(0, 1), "none")
+    ix = bench.build_index(cfg, st)
+    st["q_dev"] = torch.from_numpy(st["qx"]).to(dev)
+    st["cb_dev"] = torch.from_numpy(st["cb"]).to(dev)
     for _ in range(3):
         ix.et_etree_topk(cfg.topk, queries=st["q_dev"], codebooks=st["cb_dev"])
     torch.cuda.synchronize()
@@ -40,8 +43,8 @@ def main():
     used = buf[:, 0] > 0
     b = buf[used].astype(np.float64)
     t0 = b[:, 0].min()
-    order = [(0, 1, "start->build"), (1, 5, "stage"), (5, 6, "level0+TMEM"), (6, 7, "levels 1..6"),
-             (7, 2, "last level"), (2, 3, "scan"), (3, 4, "compaction")]
+    order = [(0, 1, "start->build"), (1, 5, "stage"), (5, 6, "round 0"), (6, 7, "TMEM copy"),
+             (7, 2, "round 1"), (2, 3, "scan"), (3, 4, "compaction")]
     print(f"units {used.sum()}  kernel span {(b[:, 4].max() - t0) / 1e3:.1f} us")
     for i, j, name in order:
         d = (b[:, j] - b[:, i]) / 1e3

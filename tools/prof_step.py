@@ -21,12 +21,14 @@ def main():
     import torch
     from paper_1509_05186_b200 import build, synth
     build.build()
-    cfg = bench.workload_config(a.config)
+    cfg = synth.CONFIGS[a.config]
     if a.Q:
         cfg = synth.scaled(cfg, Q=a.Q)
     dev = torch.device("cuda", 0)
-    st = bench.prepare_ours(cfg, dev, 0, 1)
-    ix = st["ix"]
+    st = bench.prepare(cfg, {}, bench.CudaBackend(dev), bench.Comm(0, 1), "none")
+    ix = bench.build_index(cfg, st)
+    st["q_dev"] = torch.from_numpy(st["qx"]).to(dev)
+    st["cb_dev"] = torch.from_numpy(st["cb"]).to(dev)
     for _ in range(a.steps):
         if cfg.ivf_nlist:
             d, i = ix.et_ivf_topk(st["q_dev"], nprobe=cfg.ivf_nprobe, k=cfg.topk)
