@@ -655,13 +655,15 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   return pl;
 }
 
-// IVF: chunks are (cell, <= 32 probing queries); their number is data
-// dependent, bounded by ceil(Q*w/32) + nlist (one partial chunk per cell).
+// IVF: chunks are (tier, cell, <= 32 probing queries) -- tier 0 = each
+// query's nearest probe, scanned first (kernels.cu, ivf_entry); their number
+// is data dependent, bounded by ceil(Q*w/32) + 2*nlist (one partial chunk per
+// (tier, cell)).
 static Plan make_ivf_plan(const et_index* ix, int64_t Q, int w, int k) {
   Plan pl;
   pl.MTmax = ix->M;
   pl.lut0 = (pl.MTmax == 8);
-  pl.n_chunks = (int)((Q * w + 31) / 32 + ix->nlist);
+  pl.n_chunks = (int)((Q * w + 31) / 32 + 2 * ix->nlist);   // one partial chunk per (tier, cell)
   pl.S = 1;
   pl.n_units = pl.n_chunks;
   pl.B = topk_B(std::max(1, k));
@@ -719,9 +721,9 @@ struct IvfWork {
 static IvfWork carve_ivf(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, int w) {
   IvfWork v{};
   v.probes = c.take<int32_t>((size_t)Q * w);
-  v.cell_cnt = c.take<int>(ix->nlist);
+  v.cell_cnt = c.take<int>(2 * ix->nlist);
   v.pair_pos = c.take<int>((size_t)Q * w);
-  v.chunk_off = c.take<int>(ix->nlist + 1);
+  v.chunk_off = c.take<int>(2 * ix->nlist + 1);
   v.n_chunks = c.take<int>(1);
   v.chunk_cell = c.take<int>(pl.n_chunks);
   v.chunk_lo = c.take<uint32_t>(pl.n_chunks);

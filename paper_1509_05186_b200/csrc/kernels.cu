@@ -1082,9 +1082,19 @@ cudaError_t launch_probe(const float* cT, int nlist, int d, const float* queries
 // IVF pair bucketing: (query, probe) pairs grouped by cell into chunks of 32
 // lanes so a warp scans one list's tree for 32 residual tables at once.
 // ---------------------------------------------------------------------------
-__global__ void ivf_count_kernel(const int32_t* __restrict__ probes, int64_t P, int* cell_cnt, int* pair_pos) {
+// Pairs are bucketed by (tier, cell): tier 0 holds every query's nearest
+// probe (rank 0), tier 1 the other probes.  Tier-0 chunks come first in the
+// chunk order, so the scan of a query's nearest list -- where its nearest
+// codes most likely are -- runs in the first waves and leaves a tight k-th
+// distance bound in qthr for the query's other probes.
+__device__ __forceinline__ int ivf_entry(const int32_t* probes, int64_t i, int w, int nlist) {
+  return ((i % w) == 0 ? 0 : nlist) + probes[i];
+}
+
+__global__ void ivf_count_kernel(const int32_t* __restrict__ probes, int64_t P, int w, int nlist, int* cell_cnt,
+                                 int* pair_pos) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < P) pair_pos[i] = atomicAdd(&cell_cnt[probes[i]], 1);
+  if (i < P) pair_pos[i] = atomicAdd(&cell_cnt[ivf_entry(probes, i, w, nlist)], 1);
 }
 
 __global__ void __launch_bounds__(1024) ivf_chunks_kernel(const int* __restrict__ cell_cnt, int nlist,
@@ -1093,8 +1103,9 @@ __global__ void __launch_bounds__(1024) ivf_chunks_kernel(const int* __restrict_
                                                           uint32_t* chunk_lo, uint32_t* chunk_hi) {
   __shared__ int part[1024];
   const int t = threadIdx.x;
-  const int per = (nlist + blockDim.x - 1) / blockDim.x;
-  const int c0 = min(nlist, t * per), c1 = min(nlist, c0 + per);
+  const int ne = 2 * nlist;                           // (tier, cell) entries, tier-major
+  const int per = (ne + blockDim.x - 1) / blockDim.x;
+  const int c0 = min(ne, t * per), c1 = min(ne, c0 + per);
   int loc = 0;
   for (int c = c0; c < c1; ++c) loc += (cell_cnt[c] + 31) >> 5;
   part[t] = loc;
@@ -1109,21 +1120,23 @@ __global__ void __launch_bounds__(1024) ivf_chunks_kernel(const int* __restrict_
   for (int c = c0; c < c1; ++c) {
     chunk_off[c] = run;
     const int nc = (cell_cnt[c] + 31) >> 5;
+    const int cell = c < nlist ? c : c - nlist;
     for (int j = 0; j < nc; ++j) {
-      chunk_cell[run + j] = c;
-      chunk_lo[run + j] = list_leaf_off[c];
-      chunk_hi[run + j] = list_leaf_off[c + 1];
+      chunk_cell[run + j] = cell;
+      chunk_lo[run + j] = list_leaf_off[cell];
+      chunk_hi[run + j] = list_leaf_off[cell + 1];
     }
     run += nc;
   }
-  if (t == blockDim.x - 1) { chunk_off[nlist] = part[t]; *n_chunks = part[t]; }
+  if (t == blockDim.x - 1) { chunk_off[ne] = part[t]; *n_chunks = part[t]; }
 }
 
-__global__ void ivf_scatter_kernel(const int32_t* __restrict__ probes, int64_t Q, int w, const int* __restrict__ pair_pos,
+__global__ void ivf_scatter_kernel(const int32_t* __restrict__ probes, int64_t Q, int w, int nlist,
+                                   const int* __restrict__ pair_pos,
                                    const int* __restrict__ chunk_off, int* chunk_q, int* qslot_off, int* qslot) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < Q * w) {
-    const int c = probes[i];
+    const int c = ivf_entry(probes, i, w, nlist);
     const int p = pair_pos[i];
     const int ch = chunk_off[c] + (p >> 5);
     const int ln = p & 31;
@@ -1138,14 +1151,14 @@ cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist
                               uint32_t* chunk_lo, uint32_t* chunk_hi, int* chunk_q, int max_chunks,
                               int* qslot_off, int* qslot, cudaStream_t st) {
   cudaError_t e;
-  if ((e = cudaMemsetAsync(cell_cnt, 0, (size_t)nlist * 4, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(cell_cnt, 0, (size_t)2 * nlist * 4, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(chunk_q, 0xff, (size_t)max_chunks * 32 * 4, st)) != cudaSuccess) return e;
   const int64_t P = Q * w;
-  ivf_count_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(probes, P, cell_cnt, pair_pos);
+  ivf_count_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(probes, P, w, nlist, cell_cnt, pair_pos);
   ivf_chunks_kernel<<<1, 1024, 0, st>>>(cell_cnt, nlist, list_leaf_off, chunk_off, n_chunks, chunk_cell,
                                         chunk_lo, chunk_hi);
   const int64_t n = (P > Q + 1) ? P : Q + 1;
-  ivf_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(probes, Q, w, pair_pos, chunk_off, chunk_q,
+  ivf_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(probes, Q, w, nlist, pair_pos, chunk_off, chunk_q,
                                                                    qslot_off, qslot);
   count_launch(3);
   return cudaGetLastError();

@@ -1357,9 +1357,13 @@ template <int SS, int MTC, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant__ ScanParams p) {
   constexpr bool FOREST = (MODE == 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int unit = blockIdx.x;
-  const int chunk = unit / p.S;
-  const int seg = unit - chunk * p.S;
+  // Segment-major launch order: every chunk's first segment runs in the first
+  // waves, so later segments start from the per-query bound they left in
+  // qthr.  The unit (candidate buffers, scratch) stays chunk * S + seg.
+  const int n_ch = p.n_units / p.S;
+  const int seg = (int)blockIdx.x / n_ch;
+  const int chunk = (int)blockIdx.x - seg * n_ch;
+  const int unit = chunk * p.S + seg;
   const int lane = lane_id(), warp = warp_id();
   if (threadIdx.x == 0 && smem_u32(smem_raw) != kDsmBase) __trap();   // tab_ld's fixed base
   phase_mark(unit, 0);
@@ -1401,7 +1405,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     } else {
       sm.qidx[lane] = __ldg(p.chunk_q + (size_t)chunk * 32 + lane);
     }
-    sm.thr[lane] = 0x7f800000u;   // +inf
+    // the query's bound from the units that finished before this one started
+    // (qthr: the min of proven k-th distance bounds; 0x7f7f7f7f = none yet)
+    const int q = sm.qidx[lane];
+    sm.thr[lane] = (p.qthr && p.mode == kModeTopk && q >= 0) ? min(0x7f800000u, __ldcg(p.qthr + q)) : 0x7f800000u;
   }
   __syncthreads();
   if (use_tmem) {
@@ -1423,7 +1430,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
   e.q = sm.qidx[lane];
   e.part = p.partials ? p.partials + (size_t)unit * p.part_stride : nullptr;
   e.ts.active = lane < nq;
-  e.ts.thr = e.ts.active ? __int_as_float(0x7f800000) : -1.0f;
+  e.ts.thr = e.ts.active ? __uint_as_float(sm.thr[lane]) : -1.0f;
   e.ts.cnt = 0;
   e.ts.msum = 0;
   e.ts.warp_buf = nullptr;
