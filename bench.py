@@ -794,6 +794,34 @@ def run_ours(args):
                           "queries split across ranks: tables and scans split, no collective" if mode == "queries"
                           else "lists split across ranks (LPT); residual tables built for the owned lists")}
 
+    # same-box naive-ADC arm: the same queries through a flat
+    # index of the same codes (one leaf per code, LCP 0: N*M lookups) on the
+    # same kernels; the E-Tree/E-Forest step vs this is the paper's comparison
+    flat = None
+    if (world == 1 and not args.no_flat and not ivf and not full and cfg.M <= 8 and ix is not None
+            and cfg.N <= 10_000_000):
+        fx = api.Index.et_build_flat(st["codes"], ids=st["ids"])
+        fd = torch.empty_like(dist_out)
+        fi = torch.empty_like(ids_out)
+        for _ in range(2):
+            fx.et_etree_topk(k, queries=qd, codebooks=cbd, out=(fd, fi))
+        f_evs = [(ev(), ev()) for _ in range(max(3, min(args.steps, 10)))]
+        torch.cuda.synchronize()
+        for a_, b_ in f_evs:
+            flush.fill_(1.0)
+            a_.record()
+            fx.et_etree_topk(k, queries=qd, codebooks=cbd, out=(fd, fi))
+            b_.record()
+        torch.cuda.synchronize()
+        f_ms = sum(a_.elapsed_time(b_) for a_, b_ in f_evs) / len(f_evs)
+        same = bool(torch.equal(fd, dist_out)) if not merged else None
+        flat = {"flat_adc_ms": f_ms, "etree_ms": step_ms, "etree_over_flat_time": step_ms / f_ms,
+                "speedup_vs_flat_adc": f_ms / step_ms, "flat_lookups_per_query": int(cfg.N * cfg.M),
+                "same_topk_distances": same,
+                "note": "flat = et_build_flat of the same codes through the same scan kernel "
+                        "(naive ADC: every code's M lookups); CUDA events, L2 flushed"}
+        del fx
+
     # per-kernel breakdown: the same steps, library events around each launch
     api.et_timing_reset()
     api.et_timing_enable(True)
@@ -928,6 +956,8 @@ def run_ours(args):
         }
         if terms is not None:
             out["per_rank"] = terms
+        if flat is not None:
+            out["flat_adc"] = flat
         if parity is not None:
             out["parity"] = parity
         if world == 1 and not args.no_cpu_baseline:
@@ -1052,6 +1082,7 @@ def main():
     ap.add_argument("--shard", default="auto", choices=["auto", "db", "queries", "lists"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-flat", action="store_true", help="skip the same-box naive-ADC (flat index) arm")
     ap.add_argument("--parity-queries", type=int, default=16)
     ap.add_argument("--dry-run", default=None, help="module[:attr] of a CPU test backend (tests/)")
     ap.add_argument("--dry-n", type=int, default=20_000)

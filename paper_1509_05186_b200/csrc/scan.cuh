@@ -951,6 +951,12 @@ __device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
 // kDsmBase (after the 1 KB the system reserves); scan_kernel traps if not.
 constexpr uint32_t kDsmBase = 0x400;
 
+// A shared-memory word by its 32-bit shared address, through cvta: the
+// compiler emits a plain LDS (no generic-window arithmetic) and can predicate it.
+__device__ __forceinline__ const float* smem_f32(uint32_t a) {
+  return reinterpret_cast<const float*>(__cvta_shared_to_generic(a));
+}
+
 
 template <int MT>
 __device__ __forceinline__ uint32_t rec_lcp(const uint4& r) {
@@ -974,31 +980,46 @@ __device__ __forceinline__ uint32_t rec_mbucket(const uint4& r) {
 // ((v0 + v1) + v2) + ... -- the Distance Context ctx[l] = ctx[l-1] + T[l][k_l]
 // of P:238-252 recomputed in registers, bit-identical to naive ADC.
 // `valid` = false makes the call a no-op on v (the padding leaf of a stream).
+// The TMEM levels' entries of a record (levels 0 and 1 of an 8-level tree:
+// columns k0 and 256 + k1): issued without waiting; the caller waits once
+// for every stream's reads (tmem_wait_all) before dc_leaf uses them.
+__device__ __forceinline__ void tmem_rec_ld(uint32_t tq, const uint4& r, uint32_t& t0, uint32_t& t1) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(t0) : "r"(tq + (r.x & 255u)));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(t1) : "r"(tq + 256u + ((r.x >> 16) & 255u)));
+}
+template <int NS>
+__device__ __forceinline__ void tmem_wait_all(uint32_t (&t0)[NS], uint32_t (&t1)[NS]) {
+  static_assert(NS == 1 || NS == 2 || NS == 4, "streams");
+  if constexpr (NS == 1) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0[0]), "+r"(t1[0]));
+  } else if constexpr (NS == 2) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0[0]), "+r"(t1[0]), "+r"(t0[1]), "+r"(t1[1]));
+  } else {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(t0[0]), "+r"(t1[0]), "+r"(t0[1]), "+r"(t1[1]), "+r"(t0[2]), "+r"(t1[2]), "+r"(t0[3]),
+                   "+r"(t1[3]));
+  }
+}
+
 template <int MT>
 __device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t pl, bool valid,
-                                         uint32_t lane4, uint32_t tq) {
+                                         uint32_t lane4, uint32_t t0, uint32_t t1) {
   constexpr int lv0 = lv0_of(MT);
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
   const uint32_t plv = valid ? pl : 255u;   // 255: no level is looked up
   if constexpr (lv0 == 2) {
-    // levels 0 and 1 (TMEM, columns k0 and 256 + k1) only on a new subtree at
-    // depth 0 / <= 1: warp-uniform predicates
-    uint32_t t0 = __float_as_uint(v[0]), t1 = __float_as_uint(v[1]);
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.u32 q, %2, 0;\n\t"
-                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
-                 : "+r"(t0) : "r"(tq + (w[0] & 255u)), "r"(plv));
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.le.u32 q, %2, 1;\n\t"
-                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
-                 : "+r"(t1) : "r"(tq + 256u + ((w[0] >> 16) & 255u)), "r"(plv));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0), "+r"(t1));
-    v[0] = __uint_as_float(t0);
-    v[1] = __uint_as_float(t1);
+    // levels 0 and 1 (TMEM, columns k0 and 256 + k1, read by the caller: t0,
+    // t1) take effect only on a new subtree at depth 0 / <= 1 -- otherwise
+    // the read returned the very entry the path already holds
+    if (plv == 0) v[0] = __uint_as_float(t0);
+    if (plv <= 1) v[1] = __uint_as_float(t1);
   }
 #pragma unroll
   for (int l = lv0; l < MT; ++l) {
     const uint32_t off = (l & 1) ? ((w[l >> 1] >> 16) ^ lane4) : ((w[l >> 1] & 0xffffu) ^ lane4);
-    // predicated LDS (the compiler's predicate: no shared-memory access when off)
-    if (plv <= (uint32_t)l) v[l] = *reinterpret_cast<const float*>(et_dsm + off + ((uint32_t)(l - lv0) << 15));
+    // predicated LDS at a 32-bit shared address (the compiler's predicates,
+    // moved in bulk with R2P; no shared-memory access when off)
+    if (plv <= (uint32_t)l) v[l] = *smem_f32(off + (kDsmBase + ((uint32_t)(l - lv0) << 15)));
   }
   float s = v[0];
 #pragma unroll
@@ -1030,36 +1051,37 @@ __device__ __forceinline__ uint32_t rec_mbucket_m(const uint4& r) {
 // (warp-uniform); the distance is summed per forest tree left to right and
 // the per-tree partials in tree order, ((p_0 + p_1) + ...) (reading A13):
 // bit l of `fsplit` marks the first level of tree u >= 1.
-template <int MT>
+template <int MT, int FS>
 __device__ __forceinline__ float dc_leaf_m(float (&v)[MT], const uint4& r, uint32_t mask, uint32_t lane4,
-                                           uint32_t tq, uint32_t fsplit) {
+                                           uint32_t t0, uint32_t t1, uint32_t fsplit) {
   constexpr int lv0 = lv0_of(MT);
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-  if constexpr (lv0 == 2) {
-    uint32_t t0 = __float_as_uint(v[0]), t1 = __float_as_uint(v[1]);
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
-                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
-                 : "+r"(t0) : "r"(tq + (w[0] & 255u)), "r"(mask & 1u));
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
-                 "@q tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\t}"
-                 : "+r"(t1) : "r"(tq + 256u + ((w[0] >> 16) & 255u)), "r"(mask & 2u));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0), "+r"(t1));
-    v[0] = __uint_as_float(t0);
-    v[1] = __uint_as_float(t1);
+  if constexpr (lv0 == 2) {   // TMEM levels read by the caller (t0, t1)
+    if (mask & 1u) v[0] = __uint_as_float(t0);
+    if (mask & 2u) v[1] = __uint_as_float(t1);
   }
 #pragma unroll
   for (int l = lv0; l < MT; ++l) {
     const uint32_t off = (((l & 1) ? (w[l >> 1] >> 16) : w[l >> 1]) & 0x7ffcu) ^ lane4;
-    if (mask & (1u << l)) v[l] = *reinterpret_cast<const float*>(et_dsm + off + ((uint32_t)(l - lv0) << 15));
+    if (mask & (1u << l)) v[l] = *smem_f32(off + (kDsmBase + ((uint32_t)(l - lv0) << 15)));
   }
-  float tot = 0.f, s = v[0];
-  bool have = false;
+  if constexpr (FS > 0 && FS < MT) {   // two trees split at level FS (compile time): p_0 + p_1
+    float s0 = v[0], s1 = v[FS];
 #pragma unroll
-  for (int l = 1; l < MT; ++l) {
-    if ((fsplit >> l) & 1u) { tot = have ? tot + s : s; have = true; s = v[l]; }
-    else s = s + v[l];
+    for (int l = 1; l < FS; ++l) s0 = s0 + v[l];
+#pragma unroll
+    for (int l = FS + 1; l < MT; ++l) s1 = s1 + v[l];
+    return s0 + s1;
+  } else {
+    float tot = 0.f, s = v[0];
+    bool have = false;
+#pragma unroll
+    for (int l = 1; l < MT; ++l) {
+      if ((fsplit >> l) & 1u) { tot = have ? tot + s : s; have = true; s = v[l]; }
+      else s = s + v[l];
+    }
+    return have ? tot + s : s;
   }
-  return have ? tot + s : s;
 }
 
 // Scan of leaves [a, b) of one tree by one warp, lane = query.  The range is
@@ -1134,8 +1156,14 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
         const bool ok1 = j < n1;
         const uint32_t pl0 = (off + j == 0) ? 0u : rec_lcp<MT>(r0);   // range starts: rebuild the path
         const uint32_t pl1 = (off + j == 0) ? 0u : rec_lcp<MT>(r1);
-        const float d0 = dc_leaf<MT>(v0, r0, pl0, true, lane4, tq);
-        const float d1 = dc_leaf<MT>(v1, r1, pl1, ok1, lane4, tq);
+        uint32_t t0[2] = {0u, 0u}, t1[2] = {0u, 0u};
+        if constexpr (lv0_of(MT) == 2) {
+          tmem_rec_ld(tq, r0, t0[0], t1[0]);
+          tmem_rec_ld(tq, r1, t0[1], t1[1]);
+          tmem_wait_all<2>(t0, t1);
+        }
+        const float d0 = dc_leaf<MT>(v0, r0, pl0, true, lane4, t0[0], t1[0]);
+        const float d1 = dc_leaf<MT>(v1, r1, pl1, ok1, lane4, t0[1], t1[1]);
         emit(leaf0, d0, r0, true);
         emit(leaf1, d1, r1, ok1);
       }
@@ -1153,7 +1181,7 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
 // four shuffles per leaf; a leaf costs (MT - LCP) shared-memory / TMEM
 // lookups (masked records: the levels of its mask), MT - 1 FADDs and a
 // predicated emit.
-template <int MT, bool MASKED, bool TOPK, int NS>
+template <int MT, bool MASKED, bool TOPK, int NS, int FS>
 __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b) {
   const ScanParams& p = *e.p;
   const int lane = lane_id();
@@ -1200,15 +1228,25 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
     const int n = (int)min(32u, steps - off);
     for (int j = 0; j < n; ++j) {
       const bool first = (off + j == 0);             // range start: rebuild the path
+      uint4 rr[NS];
+      uint32_t t0[NS], t1[NS];                       // TMEM levels: every stream's reads, one wait
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        rr[k] = shfl_rec(cur[k], j);
+        t0[k] = t1[k] = 0u;
+        if constexpr (lv0_of(MT) == 2) tmem_rec_ld(tq, rr[k], t0[k], t1[k]);
+      }
+      if constexpr (lv0_of(MT) == 2) tmem_wait_all<NS>(t0, t1);
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
         const bool ok = off + j < sl[k];
-        const uint4 r = shfl_rec(cur[k], j);
+        const uint4 r = rr[k];
         float dist;
         if constexpr (MASKED) {
-          dist = dc_leaf_m<MT>(v[k], r, ok ? (first ? kAll : rec_mask<MT>(r)) : 0u, lane4, tq, p.fsplit);
+          dist = dc_leaf_m<MT, FS>(v[k], r, ok ? (first ? kAll : rec_mask<MT>(r)) : 0u, lane4, t0[k], t1[k],
+                                   p.fsplit);
         } else {
-          dist = dc_leaf<MT>(v[k], r, first ? 0u : rec_lcp<MT>(r), ok, lane4, tq);
+          dist = dc_leaf<MT>(v[k], r, first ? 0u : rec_lcp<MT>(r), ok, lane4, t0[k], t1[k]);
         }
         const uint32_t lf = s0[k] + off + j;
         if constexpr (!TOPK) {
@@ -1242,8 +1280,15 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
 template <int MT, bool MASKED>
 __device__ __forceinline__ void scan_tree3_mode(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a,
                                                 uint32_t b) {
-  if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, kStreams>(e, sm, tr, a, b);
-  else scan_tree3<MT, MASKED, false, kStreams>(e, sm, tr, a, b);
+  // fused forests of two 4-level trees (the c5 split 0-3 | 4-7): the tree
+  // boundary at compile time
+  if (MASKED && MT == 8 && e.p->fsplit == (1u << 4)) {
+    if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, kStreams, 4>(e, sm, tr, a, b);
+    else scan_tree3<MT, MASKED, false, kStreams, 4>(e, sm, tr, a, b);
+    return;
+  }
+  if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, kStreams, 0>(e, sm, tr, a, b);
+  else scan_tree3<MT, MASKED, false, kStreams, 0>(e, sm, tr, a, b);
 }
 
 template <bool MASKED>
