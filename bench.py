@@ -477,13 +477,20 @@ def cpu_info():
 
 
 _ADC_CODES = None   # set before the fork pool starts (inherited, not pickled)
+_ADC_CHUNK = 1 << 22   # codes per oracle call: bounded temporaries at N = 1e8
+
+
+def _adc_chunked(tables, codes):
+    """The oracle's naive ADC (pq.adc) over all codes, a chunk of codes per call."""
+    from oracle import pq
+    for s in range(0, len(codes), _ADC_CHUNK):
+        pq.adc(tables, codes[s:s + _ADC_CHUNK])
 
 
 def _adc_worker(tables):
     """Pool worker (all-cores mode): naive ADC of the given queries' tables."""
-    from oracle import pq
     t = time.perf_counter()
-    pq.adc(tables, _ADC_CODES)
+    _adc_chunked(tables, _ADC_CODES)
     return time.perf_counter() - t
 
 
@@ -510,7 +517,7 @@ def cpu_baseline(cfg, st, budget_s=15.0):
     t = time.perf_counter()
     n = 0
     while True:
-        pq.adc(tabs[n % 64:n % 64 + 1], codes)
+        _adc_chunked(tabs[n % 64:n % 64 + 1], codes)
         n += 1
         el = time.perf_counter() - t
         if el >= per or n >= len(qx):
@@ -536,8 +543,11 @@ def cpu_baseline(cfg, st, budget_s=15.0):
     global _ADC_CODES
     _ADC_CODES = codes
     cores = os.cpu_count() or 1
-    nq = int(min(64 * cores, max(4 * cores, per * adc1 * cores / N)))
-    tabs = [pq.lut64(cb, qx[(4 * i) % len(qx):(4 * i) % len(qx) + 4]) for i in range(max(1, nq // 4))]
+    qpc = 4 if N < 10_000_000 else 1          # queries per pool task
+    nq = int(min(64 * cores, max(qpc * cores, per * adc1 * cores / N)))
+    if N >= 10_000_000:
+        nq = cores                            # one query per core (each is >= 1e7 codes)
+    tabs = [pq.lut64(cb, qx[(qpc * i) % len(qx):(qpc * i) % len(qx) + qpc]) for i in range(max(1, nq // qpc))]
     t = time.perf_counter()
     with mp.get_context("fork").Pool(cores) as pool:
         pool.map(_adc_worker, tabs, chunksize=1)
@@ -669,7 +679,11 @@ def run_ours(args):
         raise SystemExit("full output (c1) cannot be database-sharded: use --shard queries")
     backend = CudaBackend(dev)
     st = prepare(cfg, {}, backend, comm, mode)
+    t_b = time.time()
     ix = build_index(cfg, st)
+    torch.cuda.synchronize()
+    build_s = time.time() - t_b
+    log(f"[rank {rank}] index built in {build_s:.2f}s (GPU sort + group, host trees over the distinct codes)")
     stats = ix.stats() if ix is not None else []
     kk = max(k, 1)
     # this rank's queries
@@ -938,6 +952,7 @@ def run_ours(args):
                        "N": cfg.N, "d": cfg.d, "M": cfg.M, "K": cfg.K, "Q": Q, "k": k,
                        "forest_split": cfg.forest_split, "parallelism": par, "shard_mode": mode,
                        "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+                       "index_build_s": round(build_s, 3),
                        "timing": ("CUDA graph replay of one step, CUDA events per step" if world == 1
                                   else "CUDA events per step, max over ranks")},
             "roofline": roof,

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(OUT_DIR, "libetree.so")
-SOURCES = ["scan_s16.cu", "scan_s60.cu", "scan_s0.cu", "kernels.cu", "host.cpp"]
+SOURCES = ["scan_s16.cu", "scan_s60.cu", "scan_s0.cu", "kernels.cu", "build_gpu.cu", "host.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -117,6 +117,7 @@ struct DevBuf {
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
   void reset() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+  void adopt(void* ptr, size_t n) { reset(); p = ptr; bytes = n; }   // device memory made elsewhere
 };
 
 enum Kind { kTree = 0, kIvf = 1, kFlat = 2 };
@@ -398,17 +399,44 @@ static et_index* build_forest(const uint8_t* codes_in, const int32_t* ids, int64
   for (int t = 0; t <= T; ++t) ix->split[t] = split[t];
   if (!g_dry_run) cudaGetDevice(&ix->device);
   set_layers(ix.get(), byte_perm);
-  std::vector<uint8_t> pc = permute_codes(codes_in, n, M, byte_perm);
-  const uint8_t* codes = pc.data();
 
-  // full-code sort -> groups (distinct full codes, in lexicographic order)
-  std::vector<uint32_t> order = sort_slots(codes, n, M, 0, M);
-  Groups g = make_groups(codes, M, order, ids, 0, M);
+  // full-code sort -> groups (distinct full codes, in lexicographic order):
+  // on the GPU when there is one (build_gpu.cu: radix sort + flag scan; the
+  // per-id arrays stay on the device), else on the host (et_build_stats).
+  // The trees are then built from one (permuted) code row per group.
+  Groups g;
+  std::vector<uint8_t> reps;
+  if (!g_dry_run) {
+    GpuGroups gg;
+    cuda_check(gpu_group_codes(codes_in, ids, n, M, byte_perm, nullptr, &gg), "GPU index build (sort + group)");
+    const size_t G0 = (size_t)gg.G;
+    ix->n_groups = (int64_t)G0;
+    ix->ids.adopt(gg.ids, (size_t)n * 4);
+    ix->group_off.adopt(gg.group_off, (G0 + 1) * 4);
+    ix->group_mult.adopt(gg.mult, G0 * 4);
+    ix->group_minid.adopt(gg.minid, G0 * 4);
+    ix->slot2group.adopt(gg.slot2group, (size_t)n * 4);
+    g.off = std::move(gg.off);
+    reps.resize(G0 * M);
+    for (size_t j = 0; j < G0; ++j)
+      for (int l = 0; l < M; ++l) reps[j * M + l] = codes_in[(size_t)gg.first[j] * M + (byte_perm ? byte_perm[l] : l)];
+  } else {
+    std::vector<uint8_t> pc = permute_codes(codes_in, n, M, byte_perm);
+    std::vector<uint32_t> order = sort_slots(pc.data(), n, M, 0, M);
+    Groups hg = make_groups(pc.data(), M, order, ids, 0, M);
+    const size_t G0 = hg.off.size() - 1;
+    std::vector<uint32_t> slot2group(n);
+    for (size_t j = 0; j < G0; ++j)
+      for (uint32_t i = hg.off[j]; i < hg.off[j + 1]; ++i) slot2group[order[i]] = (uint32_t)j;
+    upload_groups(ix.get(), hg, slot2group);
+    reps.resize(G0 * M);
+    for (size_t j = 0; j < G0; ++j) std::memcpy(&reps[j * M], &pc[(size_t)hg.first[j] * M], M);
+    g.off = std::move(hg.off);
+  }
   const size_t G = g.off.size() - 1;
-  std::vector<uint32_t> slot2group(n);
-  for (size_t j = 0; j < G; ++j)
-    for (uint32_t i = g.off[j]; i < g.off[j + 1]; ++i) slot2group[order[i]] = (uint32_t)j;
-  upload_groups(ix.get(), g, slot2group);
+  g.first.resize(G);
+  std::iota(g.first.begin(), g.first.end(), 0u);   // row j of `reps` is group j's code
+  const uint8_t* codes = reps.data();
 
   double look = 0;
   // tree 0: groups sorted by full code are sorted by the tree-0 projection too
@@ -443,8 +471,8 @@ static et_index* build_forest(const uint8_t* codes_in, const int32_t* ids, int64
   // trees 1..T-1: distinct projections, sorted; tuple -> leaf
   for (int t = 1; t < T; ++t) {
     const int b0 = split[t], b1 = split[t + 1];
-    std::vector<uint32_t> reps(g.first.begin(), g.first.end());
-    std::vector<uint32_t> so = sort_slots(codes, n, M, b0, b1, &reps);
+    std::vector<uint32_t> rows(g.first.begin(), g.first.end());
+    std::vector<uint32_t> so = sort_slots(codes, (int64_t)G, M, b0, b1, &rows);
     // group id of each rep (rep -> position in g.first): use slot2group
     HostTree h;
     h.MT = b1 - b0; h.layer0 = b0;
@@ -457,7 +485,7 @@ static et_index* build_forest(const uint8_t* codes_in, const int32_t* ids, int64
         h.lcp.push_back(i == 0 ? 0 : (uint8_t)row_lcp(codes, M, so[i - 1], r, b0, b1));
         h.mult.push_back(0);
       }
-      const uint32_t grp = slot2group[r];
+      const uint32_t grp = r;   // row r of `reps` is group r
       tup_leaf[grp] = (uint32_t)(h.code.size() - 1);
       h.mult.back() += g.off[grp + 1] - g.off[grp];
     }
@@ -533,49 +561,45 @@ static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t 
   ix->split[0] = 0; ix->split[1] = M;
   cudaGetDevice(&ix->device);
   set_layers(ix.get(), nullptr);
-  // bucket slots by list (stable), then sort each list by code
-  std::vector<std::vector<uint32_t>> members(nlist);
-  for (int64_t i = 0; i < n; ++i) members[list_of[i]].push_back((uint32_t)i);
+  // (list, code) groups in (list, code) order on the GPU (build_gpu.cu); one
+  // tree per list over its distinct codes, LCPs restart at every list
+  GpuGroups gg;
+  cuda_check(gpu_group_codes(codes_in, ids, n, M, nullptr, list_of, &gg), "GPU index build (sort + group)");
+  const size_t G = (size_t)gg.G;
+  ix->n_groups = (int64_t)G;
+  ix->ids.adopt(gg.ids, (size_t)n * 4);
+  ix->group_off.adopt(gg.group_off, (G + 1) * 4);
+  ix->group_mult.adopt(gg.mult, G * 4);
+  ix->group_minid.adopt(gg.minid, G * 4);
+  ix->slot2group.adopt(gg.slot2group, (size_t)n * 4);
   HostTree h;
   h.MT = M;
-  Groups g;
-  std::vector<uint32_t> s2g(n);
   ix->list_leaf_off.assign(nlist + 1, 0);
   et_tree_stats tot{};
+  size_t j = 0;
   for (int c = 0; c < nlist; ++c) {
     ix->list_leaf_off[c] = (uint32_t)h.code.size();
-    if (members[c].empty()) continue;
-    std::vector<uint32_t> so = sort_slots(codes_in, n, M, 0, M, &members[c]);
     HostTree lt;
     lt.MT = M;
-    for (size_t i = 0; i < so.size(); ++i) {
-      const uint32_t r = so[i];
-      const bool newleaf = (i == 0) || !rows_equal(codes_in, M, so[i - 1], r, 0, M);
-      if (newleaf) {
-        const uint64_t pk = pack(codes_in + (size_t)r * M, 0, M);
-        const uint8_t lp = i == 0 ? 0 : (uint8_t)row_lcp(codes_in, M, so[i - 1], r, 0, M);
-        lt.code.push_back(pk); lt.lcp.push_back(lp); lt.mult.push_back(0);
-        h.code.push_back(pk); h.lcp.push_back(lp); h.mult.push_back(0);
-        g.off.push_back((uint32_t)g.ids.size());
-        g.first.push_back(r);
-      }
-      lt.mult.back() += 1;
-      h.mult.back() += 1;
-      s2g[r] = (uint32_t)(h.code.size() - 1);
-      g.ids.push_back(ids ? ids[r] : (int32_t)r);
+    int64_t nc = 0;
+    for (; j < G && list_of[gg.first[j]] == c; ++j) {
+      const uint32_t r = gg.first[j];
+      const uint64_t pk = pack(codes_in + (size_t)r * M, 0, M);
+      const uint8_t lp = lt.code.empty() ? 0 : (uint8_t)row_lcp(codes_in, M, gg.first[j - 1], r, 0, M);
+      const uint64_t mu = gg.off[j + 1] - gg.off[j];
+      lt.code.push_back(pk); lt.lcp.push_back(lp); lt.mult.push_back(mu);
+      h.code.push_back(pk); h.lcp.push_back(lp); h.mult.push_back(mu);
+      nc += (int64_t)mu;
     }
-    tree_stats(lt, (int64_t)so.size());
+    if (lt.code.empty()) continue;
+    tree_stats(lt, nc);
     tot.L1 += lt.st.L1; tot.L2 += lt.st.L2; tot.total_postfix += lt.st.total_postfix;
     tot.lookups += lt.st.lookups; tot.L2_records += lt.st.L2_records; tot.paper_bytes += lt.st.paper_bytes;
   }
+  if (j != G) fail(ET_ERR_CORRUPT, "internal: IVF groups out of list order");
   ix->list_leaf_off[nlist] = (uint32_t)h.code.size();
-  g.off.push_back((uint32_t)g.ids.size());
-  if (ids) {
-    for (size_t j = 0; j + 1 < g.off.size(); ++j) std::sort(g.ids.begin() + g.off[j], g.ids.begin() + g.off[j + 1]);
-  }
-  upload_groups(ix.get(), g, s2g);
   tot.N = n; tot.M = M; tot.device_bytes = (int64_t)h.code.size() * 16;
-  tot.groups = (int64_t)(g.off.size() - 1);
+  tot.groups = (int64_t)G;
   ix->n_leaves[0] = (int64_t)h.code.size();
   ix->code[0].upload(make_records(h));
   ix->lcp[0].upload(h.lcp);
@@ -1017,7 +1041,12 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   fp.out_dist = dist; fp.out_ids = ids;
   // register fast path when groups are large (few candidates per query)
   fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
+  // small groups (many candidates): the scan kernel merges each query's
+  // per-warp lists into one and cuts it to its exact unit top-k, so the
+  // finalize reads one list per unit; large groups (few candidates) keep the
+  // per-warp lists (the in-CTA merge costs ~5 us per CTA on c2)
   sp.compact = !fp.fast;
+  fp.lpu = sp.compact ? 1 : kWarps;
   // (a finalize fused into the scan kernel was measured +30 us on c2: its
   // latency-bound tail runs with the SM otherwise idle)
   cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
@@ -1074,7 +1103,8 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   sp.qthr = w.qthr;
   sp.qthr_shared = 1;
   cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, st), "qthr init");
-  sp.compact = !((double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0));   // = !fp.fast
+  const bool ivf_fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
+  sp.compact = !ivf_fast;
   cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(ivf)");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
@@ -1087,7 +1117,8 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   fp.unit_thr = w.unit_thr;
   fp.qthr = w.qthr;
   fp.out_dist = dist; fp.out_ids = ids;
-  fp.fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
+  fp.fast = ivf_fast;
+  fp.lpu = sp.compact ? 1 : kWarps;
   cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
   ET_API_END
 }

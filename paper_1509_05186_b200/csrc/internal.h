@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 namespace et {
 
 constexpr int kWarps = 8;                  // warps per scan CTA (1 CTA / SM: the tables fill smem; 255 registers)
@@ -37,6 +39,7 @@ struct TreeDev {
 struct FinParams {
   int64_t Q = 0;
   int k = 0, B = 0, S = 1;
+  int lpu = kWarps;                   // candidate lists per unit (1: compacted by the scan kernel)
   const int* qslot_off = nullptr;     // [Q+1]
   const int* qslot = nullptr;         // chunk*32 + lane for each (query, probe)
   int flat_nchunks = 0;               // > 0: one slot per query, computed from the flat chunking
@@ -152,5 +155,22 @@ cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist
 cudaError_t launch_merge(const float* in_dist, const int32_t* in_ids, int G, int64_t Q, int k,
                          float* out_dist, int32_t* out_ids, cudaStream_t st);
 void count_launch(int n = 1);
+
+// GPU grouping step of the index build (build_gpu.cu): codes sorted
+// lexicographically (byte order `perm`), ids ascending within equal codes;
+// G groups of identical codes (IVF: of identical (list, code) pairs).  Device arrays (owned by the caller after the
+// call): ids [n] grouped, group_off [G+1], mult [G], minid [G], slot2group [n].
+// Host: off [G+1], first [G] = one slot of each group.
+struct GpuGroups {
+  int64_t G = 0;
+  std::vector<uint32_t> off, first;
+  int32_t* ids = nullptr;
+  uint32_t* group_off = nullptr;
+  uint32_t* mult = nullptr;
+  int32_t* minid = nullptr;
+  uint32_t* slot2group = nullptr;
+};
+cudaError_t gpu_group_codes(const uint8_t* codes_h, const int32_t* ids_h, int64_t n, int M, const int32_t* perm_h,
+                            const int32_t* list_h, GpuGroups* out);   // list_h: IVF (list, code) order
 
 }  // namespace et

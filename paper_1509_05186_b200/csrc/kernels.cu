@@ -76,30 +76,23 @@ struct FinWarp {                // one warp's finalize scratch (shared memory)
 __device__ __forceinline__ int fin_s0(const FinParams& p, int64_t q) { return p.flat_nchunks ? 0 : p.qslot_off[q]; }
 __device__ __forceinline__ int fin_s1(const FinParams& p, int64_t q) { return p.flat_nchunks ? 1 : p.qslot_off[q + 1]; }
 __device__ __forceinline__ int fin_slot(const FinParams& p, int64_t q, int j) {
-  if (p.flat_nchunks) {   // chunk c holds queries [c*Q/n, (c+1)*Q/n)
-    const int64_t n = p.flat_nchunks, Q = p.Q;
-    if (Q * n < (1ll << 32)) {   // 32-bit arithmetic (the common case)
-      const uint32_t Qu = (uint32_t)Q, nu = (uint32_t)n, qu = (uint32_t)q;
-      uint32_t c = (uint32_t)(((uint64_t)qu * nu) / Qu);
-      while (c + 1 < nu && (c + 1) * Qu / nu <= qu) ++c;
-      while (c > 0 && c * Qu / nu > qu) --c;
-      return (int)(c * 32 + (qu - c * Qu / nu));
-    }
-    int64_t c = q * n / Q;
-    while (c + 1 < n && (c + 1) * Q / n <= q) ++c;
-    while (c > 0 && c * Q / n > q) --c;
-    return (int)(c * 32 + (q - c * Q / n));
+  if (p.flat_nchunks) {   // chunk c holds queries [floor(cQ/n), floor((c+1)Q/n))
+    // q's chunk is the smallest c with floor((c+1)Q/n) > q, i.e.
+    // c = ceil((q+1) n / Q) - 1 = floor(((q+1) n - 1) / Q)
+    const uint64_t n = (uint64_t)p.flat_nchunks, Q = (uint64_t)p.Q, qu = (uint64_t)q;
+    const uint64_t c = ((qu + 1) * n - 1) / Q;
+    return (int)(c * 32 + (qu - c * Q / n));
   }
   return __ldg(p.qslot + j);
 }
 
-// Candidate list li of query q, 0 <= li < (s1 - s0) * S * kWarps: one per
+// Candidate list li of query q, 0 <= li < (s1 - s0) * S * lpu: one per
 // (slot, leaf segment, scan warp).  Its count is cand_cnt[list], its entries
 // cand[list * B ...] (the scan kernel's per-warp, per-lane buffers).
 __device__ __forceinline__ size_t fin_list(const FinParams& p, int64_t q, int s0, int li) {
-  const int per = p.S * kWarps;
+  const int per = p.S * p.lpu;
   const int j = li / per, r = li - j * per;
-  const int sg = r / kWarps, w = r - sg * kWarps;
+  const int sg = r / p.lpu, w = r - sg * p.lpu;
   const int slot = fin_slot(p, q, s0 + j);
   return ((size_t)((slot >> 5) * p.S + sg) * 32 + (slot & 31)) * kWarps + w;
 }
@@ -128,7 +121,7 @@ struct CandSrc {
     // 32 lists per round: counts loaded in parallel (lane = list), then the
     // round's entries spread over the lanes (binary search on the prefix)
     const uint32_t tb = __float_as_uint(thr);
-    const int nl = (s1 - s0) * p->S * kWarps;
+    const int nl = (s1 - s0) * p->S * p->lpu;
     for (int l0 = 0; l0 < nl; l0 += 32) {
       const int li = l0 + lane;
       size_t ul = 0;
@@ -194,7 +187,7 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
     uint32_t* K_ = fw.key;
     uint32_t* G_ = fw.grp;
     uint32_t* U_ = fw.mul;
-    const int nl = (s1 - s0) * p.S * kWarps;
+    const int nl = (s1 - s0) * p.S * p.lpu;
     for (int l0 = 0; l0 < nl && !overflow; l0 += 32) {
       const int li = l0 + lane;
       size_t ul = 0;
@@ -560,7 +553,7 @@ __device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t 
   uint2 r0 = make_uint2(0xffffffffu, 0), r1 = make_uint2(0xffffffffu, 0);
   int n = 0;
   bool overflow = false;
-  const int nl = (s1 - s0) * p.S * kWarps;
+  const int nl = (s1 - s0) * p.S * p.lpu;
   for (int l0 = 0; l0 < nl && !overflow; l0 += 32) {
     const int li = l0 + lane;
     size_t ul = 0;

@@ -1001,25 +1001,63 @@ __device__ __forceinline__ void tmem_wait_all(uint32_t (&t0)[NS], uint32_t (&t1)
   }
 }
 
+// Forest distance with the tree boundaries at run time (bit l of fsplit:
+// level l starts tree u >= 1): per-tree partials left to right, summed in
+// tree order (A13).
+template <int MT>
+__device__ __forceinline__ float dc_sum_forest(const float (&v)[MT], uint32_t fsplit) {
+  float tot = 0.f, s = v[0];
+  bool have = false;
+#pragma unroll
+  for (int l = 1; l < MT; ++l) {
+    if ((fsplit >> l) & 1u) { tot = have ? tot + s : s; have = true; s = v[l]; }
+    else s = s + v[l];
+  }
+  return have ? tot + s : s;
+}
+
+// The lookups of one leaf: level l's entry is (re)loaded iff bit l of
+// `look` (warp-uniform) -- the levels after the leaf's LCP (P:249, P:239,
+// P:242-243), or a fused-forest tuple's mask; the TMEM levels' entries were
+// read by the caller (t0, t1).
+template <int MT>
+__device__ __forceinline__ void dc_look(float (&v)[MT], const uint4& r, uint32_t look, uint32_t lane4, uint32_t t0,
+                                        uint32_t t1) {
+  constexpr int lv0 = lv0_of(MT);
+  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+  if constexpr (lv0 == 2) {
+    if (look & 1u) v[0] = __uint_as_float(t0);
+    if (look & 2u) v[1] = __uint_as_float(t1);
+  }
+#pragma unroll
+  for (int l = lv0; l < MT; ++l) {
+    // (bits 0..1 of a half-word are free; masked records keep no data there
+    // either: & 0x7ffc is the offset)
+    const uint32_t off = (((l & 1) ? (w[l >> 1] >> 16) : w[l >> 1]) & 0x7ffcu) ^ lane4;
+    if (look & (1u << l)) v[l] = *smem_f32(off + (kDsmBase + ((uint32_t)(l - lv0) << 15)));
+  }
+}
+
 template <int MT>
 __device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t pl, bool valid,
                                          uint32_t lane4, uint32_t t0, uint32_t t1) {
   constexpr int lv0 = lv0_of(MT);
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-  const uint32_t plv = valid ? pl : 255u;   // 255: no level is looked up
+  // levels looked up: l >= LCP, as a bit mask (the compiler turns the tests
+  // below into one R2P instead of a compare per level)
+  const uint32_t look = valid ? ((0xffu << pl) & 0xffu) : 0u;
   if constexpr (lv0 == 2) {
     // levels 0 and 1 (TMEM, columns k0 and 256 + k1, read by the caller: t0,
     // t1) take effect only on a new subtree at depth 0 / <= 1 -- otherwise
     // the read returned the very entry the path already holds
-    if (plv == 0) v[0] = __uint_as_float(t0);
-    if (plv <= 1) v[1] = __uint_as_float(t1);
+    if (look & 1u) v[0] = __uint_as_float(t0);
+    if (look & 2u) v[1] = __uint_as_float(t1);
   }
 #pragma unroll
   for (int l = lv0; l < MT; ++l) {
     const uint32_t off = (l & 1) ? ((w[l >> 1] >> 16) ^ lane4) : ((w[l >> 1] & 0xffffu) ^ lane4);
-    // predicated LDS at a 32-bit shared address (the compiler's predicates,
-    // moved in bulk with R2P; no shared-memory access when off)
-    if (plv <= (uint32_t)l) v[l] = *smem_f32(off + (kDsmBase + ((uint32_t)(l - lv0) << 15)));
+    // predicated LDS at a 32-bit shared address (no shared-memory access when off)
+    if (look & (1u << l)) v[l] = *smem_f32(off + (kDsmBase + ((uint32_t)(l - lv0) << 15)));
   }
   float s = v[0];
 #pragma unroll
@@ -1237,29 +1275,59 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
         if constexpr (lv0_of(MT) == 2) tmem_rec_ld(tq, rr[k], t0[k], t1[k]);
       }
       if constexpr (lv0_of(MT) == 2) tmem_wait_all<NS>(t0, t1);
+      // lookups of every stream, then the streams' sums interleaved level by
+      // level (independent FADD chains side by side), then the emits
+      bool ok[NS];
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        const bool ok = off + j < sl[k];
-        const uint4 r = rr[k];
-        float dist;
-        if constexpr (MASKED) {
-          dist = dc_leaf_m<MT, FS>(v[k], r, ok ? (first ? kAll : rec_mask<MT>(r)) : 0u, lane4, t0[k], t1[k],
-                                   p.fsplit);
-        } else {
-          dist = dc_leaf<MT>(v[k], r, first ? 0u : rec_lcp<MT>(r), ok, lane4, t0[k], t1[k]);
+        ok[k] = off + j < sl[k];
+        uint32_t look;
+        if constexpr (MASKED) look = ok[k] ? (first ? kAll : rec_mask<MT>(rr[k])) : 0u;
+        else look = ok[k] ? ((0xffu << (first ? 0u : rec_lcp<MT>(rr[k]))) & kAll) : 0u;
+        dc_look<MT>(v[k], rr[k], look, lane4, t0[k], t1[k]);
+      }
+      float dist[NS];
+      if constexpr (MASKED && FS > 0 && FS < MT) {   // two trees: (p_0 + p_1), each left to right (A13)
+        float s1[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) { dist[k] = v[k][0]; s1[k] = v[k][FS]; }
+#pragma unroll
+        for (int l = 1; l < MT; ++l) {
+          if (l == FS) continue;
+#pragma unroll
+          for (int k = 0; k < NS; ++k) {
+            if (l < FS) dist[k] = dist[k] + v[k][l];
+            else s1[k] = s1[k] + v[k][l];
+          }
         }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) dist[k] = dist[k] + s1[k];
+      } else if constexpr (MASKED) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) dist[k] = dc_sum_forest<MT>(v[k], p.fsplit);
+      } else {   // ((v0 + v1) + v2) + ...: the Distance Context, bit-identical to naive ADC
+#pragma unroll
+        for (int k = 0; k < NS; ++k) dist[k] = v[k][0];
+#pragma unroll
+        for (int l = 1; l < MT; ++l)
+#pragma unroll
+          for (int k = 0; k < NS; ++k) dist[k] = dist[k] + v[k][l];
+      }
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        const uint4 r = rr[k];
         const uint32_t lf = s0[k] + off + j;
         if constexpr (!TOPK) {
-          if (ok) p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + lf] = dist;   // query-major rows
+          if (ok[k]) p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + lf] = dist[k];   // query-major rows
         } else {
           TopkState& ts = e.ts;
           const uint32_t bucket = MASKED ? rec_mbucket_m<MT>(r) : rec_mbucket<MT>(r);
-          const bool em = ok && ts.active && dist <= ts.thr;
-          if (em) ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), lf);
+          const bool em = ok[k] && ts.active && dist[k] <= ts.thr;
+          if (em) ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist[k]), lf);
           ts.cnt += em ? 1 : 0;
           ts.msum += em ? (1u << bucket) : 0u;
           // one group alone (2^bucket <= multiplicity ids) bounds the k-th distance
-          if (em && (1u << bucket) >= (uint32_t)p.k) ts.thr = dist;
+          if (em && (1u << bucket) >= (uint32_t)p.k) ts.thr = dist[k];
         }
       }
     }

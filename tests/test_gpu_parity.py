@@ -315,3 +315,40 @@ def test_build_codebooks_monotone_and_close_to_oracle():
     ours = sum(h[-1] for h in hist)
     theirs = sum(h[-1] for h in ohist)
     assert abs(ours - theirs) / theirs < 0.05
+
+
+# --------------------------------------------------------------------------- GPU-native build (f1)
+
+@pytest.mark.parametrize("seed,N,M,K,nd,split,user_ids", [
+    (1, 30000, 8, 256, None, (0, 8), False),
+    (3, 40000, 8, 256, 500, (0, 8), True),        # duplicate heavy, user ids
+    (4, 20000, 16, 16, None, (0, 8, 16), False),  # joined forest (M = 16)
+    (5, 20000, 8, 4, None, (0, 4, 8), True),      # fused forest
+    (7, 25000, 6, 3, None, (0, 2, 5, 6), False),
+])
+def test_gpu_build_stats_equal_host_and_oracle(seed, N, M, K, nd, split, user_ids):
+    """The GPU grouping step (radix sort + flag scan, build_gpu.cu) yields the
+    same trees as the host build and the oracle's plain definition."""
+    from test_lib_cpu import _oracle_stats
+    codes = synth.random_codes(seed, N, M, K, nd)
+    ids = (np.random.default_rng(seed).permutation(3 * N)[:N].astype(np.int32) if user_ids else None)
+    if len(split) == 2:
+        ix = api.Index.et_build_etree(codes, ids=ids, K=K)
+    else:
+        ix = api.Index.et_build_eforest(codes, split=list(split), ids=ids, K=K)
+    got = ix.stats()
+    host = api.et_build_stats(codes, split=list(split), ids=ids, K=K)
+    ref = _oracle_stats(codes, split)
+    keys = ("L1", "L2", "total_postfix", "lookups", "L2_records", "paper_bytes", "groups", "scan_lookups")
+    for g, h, r in zip(got, host, ref):
+        assert all(g[k_] == h[k_] for k_ in keys), (g, h)
+        assert (g["L1"], g["L2"], g["total_postfix"]) == (r.L1, r.L2, r.total_postfix)
+    # the device id order (ascending within a group) through a query: top-k vs oracle
+    cb = synth.random_floats(seed + 9, (M, K, 4), 0, 5)
+    qx = synth.random_floats(seed + 10, (6, M * 4), 0, 5)
+    d, i = ix.et_etree_topk(30, queries=dev(qx), codebooks=dev(cb))
+    full = ix.et_etree_distances(queries=dev(qx), codebooks=dev(cb))
+    torch.cuda.synchronize()
+    check_topk(d.cpu().numpy(), i.cpu().numpy(), cb, qx, codes, 30, range(6), ids_map=ids)
+    ref_full = pq.adc(pq.lut64(cb, qx), codes)
+    assert rel_err(full.cpu().numpy(), ref_full).max() <= RTOL
