@@ -635,6 +635,7 @@ static int num_sms() {
 struct Plan {
   int n_chunks = 0, S = 1, n_units = 0, MTmax = 0, B = 0;
   bool lut0 = false;
+  bool mat_luts = false;   // tables materialised by lut_kernel, copied into each scan CTA
   int64_t part_stride = 0;
   int64_t part_base[kMaxTrees] = {};
 };
@@ -643,8 +644,23 @@ struct Plan {
 // one batch of emissions (kBatchEmit) before the next buffer check
 static int topk_B(int k) { return ((2 * k + kBatchEmit + 31) / 32) * 32; }
 
+// Joined forests (M > 8, e.g. c3) rebuild a tree's levels in every scan CTA
+// for few queries per CTA; their tables are cheaper built once by lut_kernel
+// at full occupancy (Q*M*K*4 bytes, L2-resident at c3's 16 MB) and copied.
+static bool materialise_tables(const et_index* ix, int64_t Q) {
+  static int mode = [] {
+    const char* e = std::getenv("ET_TABLES");
+    return !e ? 0 : (std::strcmp(e, "fused") == 0 ? 1 : (std::strcmp(e, "materialised") == 0 ? 2 : 0));
+  }();
+  if (mode == 1) return false;
+  const bool big = (double)Q * ix->M * ix->K * 4 > 512.0 * (1 << 20);
+  if (mode == 2) return !big;
+  return ix->kind == kTree && ix->T > 1 && !ix->fused && !big;
+}
+
 static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   Plan pl;
+  pl.mat_luts = materialise_tables(ix, Q);
   for (int t = 0; t < ix->T; ++t) pl.MTmax = std::max(pl.MTmax, ix->stats[t].M);
   if (ix->fused) pl.MTmax = ix->M;   // one scan over all M levels
   pl.lut0 = (pl.MTmax == 8);
@@ -707,6 +723,7 @@ struct Carve {
 };
 
 struct Work {
+  float* luts;
   int* chunk_q; int* qslot_off; int* qslot;
   float* lut0; float* partials; float* leafdist;
   uint2* cand; int* cand_cnt; float* unit_thr;
@@ -715,6 +732,7 @@ struct Work {
 
 static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool full, int slots_per_q) {
   Work w{};
+  w.luts = pl.mat_luts ? c.take<float>((size_t)Q * ix->M * ix->K) : nullptr;
   w.chunk_q = c.take<int>((size_t)pl.n_chunks * 32);
   w.qslot_off = c.take<int>(Q + 1);
   w.qslot = c.take<int>((size_t)Q * slots_per_q);
@@ -812,6 +830,16 @@ static void table_source(ScanParams& sp, const et_index* ix, const float* codebo
     sp.s = d / ix->M;
     sp.vec4 = aligned16(queries) && aligned16(codebooks) && (d % 4 == 0) ? 1 : 0;
   }
+}
+
+// Materialised-tables plan: lut_kernel writes [Q][M][K] into the workspace
+// and the scan CTAs copy their queries' rows (same arithmetic).
+static void materialise(ScanParams& sp, const et_index* ix, const Plan& pl, const Work& w, int64_t Q, cudaStream_t st) {
+  if (!pl.mat_luts || sp.luts) return;
+  const bool v4 = aligned16(sp.codebooks) && aligned16(sp.queries);
+  cuda_check(timed("luts", st, [&] { return launch_luts(sp.codebooks, sp.d, ix->M, ix->K, sp.queries, Q, w.luts, v4, st); }),
+             "luts");
+  sp.luts = w.luts;
 }
 
 }  // namespace et
@@ -984,6 +1012,7 @@ et_status et_etree_distances(const et_index* ix, const float* codebooks, int32_t
   Work w = carve(c, ix, pl, Q, true, 1);
   cudaStream_t st = (cudaStream_t)stream;
   cuda_check(timed("fill", st, [&] { return launch_fill_flat(Q, pl.n_chunks, w.chunk_q, w.qslot_off, w.qslot, st); }), "fill");
+  materialise(sp, ix, pl, w, Q, st);
   fill_scan_common(sp, ix, pl);
   sp.chunk_q = w.chunk_q;
   sp.lut0 = w.lut0;
@@ -1015,6 +1044,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   Carve c{reinterpret_cast<char*>(workspace), 0, ws};
   Work w = carve(c, ix, pl, Q, false, 1);
   cudaStream_t st = (cudaStream_t)stream;
+  materialise(sp, ix, pl, w, Q, st);
   fill_scan_common(sp, ix, pl);
   sp.flatQ = Q;   // arithmetic chunking: no fill launch
   sp.lut0 = w.lut0;

@@ -573,8 +573,11 @@ __device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t 
     constexpr int kRounds = 4;   // candidate loads of four rounds in flight at once
     for (int i00 = 0; i00 < total && !overflow; i00 += 32 * kRounds) {
       uint2 vv[kRounds];
+      const int live = (total - i00 + 31) >> 5;   // rounds with candidates (warp-uniform)
 #pragma unroll
       for (int rr = 0; rr < kRounds; ++rr) {
+        vv[rr] = make_uint2(0xffffffffu, 0);
+        if (rr >= live) continue;                  // (few candidates: one round, not four)
         const int idx = i00 + rr * 32 + lane;
         int w = 0;
 #pragma unroll
@@ -588,6 +591,7 @@ __device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t 
       }
 #pragma unroll
       for (int rr = 0; rr < kRounds; ++rr) {
+        if (rr >= live) break;
         const int idx = i00 + rr * 32 + lane;
         const uint2 v = vv[rr];
         const bool keep = (idx < total) && v.x <= tb;

@@ -318,6 +318,24 @@ __device__ __forceinline__ void build_tables_resident8(const ScanParams& p, cons
   const uint32_t stg_s = smem_u32(sm.bigstage);
   const int np = (nq + 1) >> 1;                                          // query pairs
   constexpr uint32_t pair_bytes = SS * 2 * 4;                            // 128 B per (level, pair)
+  const int lw = warp / kWPL;                         // level within the round
+  const int row0 = (warp % kWPL) * 32 * kR;           // first codeword row of this warp
+  const bool active = row0 < K;                       // K < 256: idle codeword blocks
+  auto load_cw = [&](int l, float (&c)[kR][SS]) {
+    const int m = p.lsub[tr.layer0 + l];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int k = row0 + 32 * r + lane;
+      const float* row = p.codebooks + ((size_t)m * K + (k < K ? k : 0)) * SS;
+#pragma unroll
+      for (int j = 0; j < SS; j += 4) {
+        const float4 u = __ldg(reinterpret_cast<const float4*>(row + j));
+        c[r][j] = u.x; c[r][j + 1] = u.y; c[r][j + 2] = u.z; c[r][j + 3] = u.w;
+      }
+    }
+  };
+  float c[kR][SS];
+  if (active) load_cw(lw, c);                         // round 0's rows: in flight during the staging wait
   if (staged) {
     asm volatile("cp.async.wait_all;" ::: "memory");   // this thread's stage_async copies landed
   } else {
@@ -339,22 +357,6 @@ __device__ __forceinline__ void build_tables_resident8(const ScanParams& p, cons
       for (int l = 0; l < 8; ++l) sts(stg_s + (uint32_t)l * kStageLevelBytes + o, v[l]);
     }
   }
-  const int lw = warp / kWPL;                         // level within the round
-  const int row0 = (warp % kWPL) * 32 * kR;           // first codeword row of this warp
-  const bool active = row0 < K;                       // K < 256: idle codeword blocks
-  auto load_cw = [&](int l, float (&c)[kR][SS]) {
-    const int m = p.lsub[tr.layer0 + l];
-#pragma unroll
-    for (int r = 0; r < kR; ++r) {
-      const int k = row0 + 32 * r + lane;
-      const float* row = p.codebooks + ((size_t)m * K + (k < K ? k : 0)) * SS;
-#pragma unroll
-      for (int j = 0; j < SS; j += 4) {
-        const float4 u = __ldg(reinterpret_cast<const float4*>(row + j));
-        c[r][j] = u.x; c[r][j + 1] = u.y; c[r][j + 2] = u.z; c[r][j + 3] = u.w;
-      }
-    }
-  };
   // Entries of one table (region dst_s) for this lane's kR rows and every
   // staged query pair of xs_s, two pairs per iteration.  Query slots >= nq and
   // rows >= K are written but never looked up.
@@ -420,8 +422,6 @@ __device__ __forceinline__ void build_tables_resident8(const ScanParams& p, cons
       }
     }
   };
-  float c[kR][SS];
-  if (active) load_cw(lw, c);
   __syncthreads();                                   // stage complete
   phase_mark(unit, 5);
   // round 0: level lw -> region (levels 0, 1: regions 2, 3 until the TMEM copy)
@@ -1521,7 +1521,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     // the query's bound from the units that finished before this one started
     // (qthr: the min of proven k-th distance bounds; 0x7f7f7f7f = none yet)
     const int q = sm.qidx[lane];
-    sm.thr[lane] = (p.qthr && p.mode == kModeTopk && q >= 0) ? min(0x7f800000u, __ldcg(p.qthr + q)) : 0x7f800000u;
+    // (only queries spanning several units: S > 1, IVF probes)
+    sm.thr[lane] = (p.qthr_shared && p.mode == kModeTopk && q >= 0) ? min(0x7f800000u, __ldcg(p.qthr + q))
+                                                                     : 0x7f800000u;
   }
   __syncthreads();
   if (use_tmem) {
