@@ -9,6 +9,15 @@
 
 namespace et {
 
+// Device-side bounds checks of a checked build (-DET_CHECKS, tools/
+// sanitize_cases.py): a violated check traps (the launch fails with an error
+// the host reports).  compute-sanitizer is unavailable on this pool.
+#ifdef ET_CHECKS
+#define ET_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define ET_CHECK(cond) do { } while (0)
+#endif
+
 #define FULLMASK 0xffffffffu
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

@@ -644,9 +644,10 @@ struct Plan {
 // one batch of emissions (kBatchEmit) before the next buffer check
 static int topk_B(int k) { return ((2 * k + kBatchEmit + 31) / 32) * 32; }
 
-// Joined forests (M > 8, e.g. c3) rebuild a tree's levels in every scan CTA
-// for few queries per CTA; their tables are cheaper built once by lut_kernel
-// at full occupancy (Q*M*K*4 bytes, L2-resident at c3's 16 MB) and copied.
+// Tables built once by lut_kernel ([Q][M][K] in the workspace) and copied
+// into each scan CTA, instead of built inside the CTA: ET_TABLES=materialised
+// (experiments; the default is the fused build -- on c3, whose CTAs hold ~7
+// queries, fused 136 us vs materialised 185 us of which lut_kernel 98 us).
 static bool materialise_tables(const et_index* ix, int64_t Q) {
   static int mode = [] {
     const char* e = std::getenv("ET_TABLES");
@@ -655,7 +656,7 @@ static bool materialise_tables(const et_index* ix, int64_t Q) {
   if (mode == 1) return false;
   const bool big = (double)Q * ix->M * ix->K * 4 > 512.0 * (1 << 20);
   if (mode == 2) return !big;
-  return ix->kind == kTree && ix->T > 1 && !ix->fused && !big;
+  return false;   // auto: fused (measured: c3 fused 136 us vs materialised 185 us, lut_kernel 98 us of it)
 }
 
 static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {

@@ -215,6 +215,7 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
         const int wo = __shfl_sync(FULLMASK, excl, w);
         const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
         uint2 v = make_uint2(0xffffffffu, 0);
+        ET_CHECK(idx >= total || idx - wo < p.B);
         if (idx < total) v = p.cand[ulw * p.B + (idx - wo)];
         const bool keep = (idx < total) && v.x <= tb;
         const unsigned m = __ballot_sync(FULLMASK, keep);
@@ -587,6 +588,7 @@ __device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t 
         }
         const int wo = __shfl_sync(FULLMASK, excl, w);
         const unsigned long long ulw = __shfl_sync(FULLMASK, (unsigned long long)ul, w);
+        ET_CHECK(idx >= total || idx - wo < p.B);
         vv[rr] = (idx < total) ? p.cand[ulw * p.B + (idx - wo)] : make_uint2(0xffffffffu, 0);
       }
 #pragma unroll

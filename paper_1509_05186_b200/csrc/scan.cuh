@@ -392,6 +392,7 @@ __device__ __forceinline__ void build_tables_resident8(const ScanParams& p, cons
         f2unpack(a[0][r], e0, o0);
         f2unpack(a[1][r], e1, o1);
         const uint32_t row = rows + ((uint32_t)r << 12);   // row + 32 r
+        ET_CHECK(row + 128u <= (dst_s - dsm_s) + 32768u && i4 + 12u < 128u);
         sts_off(row + ((i4 ^ sw) & 0x7cu), e0);
         sts_off(row + (((i4 + 4) ^ sw) & 0x7cu), o0);
         sts_off(row + (((i4 + 8) ^ sw) & 0x7cu), e1);
@@ -894,6 +895,7 @@ __device__ __forceinline__ void emit_group(EmitCtx& e, float dist, uint32_t g, u
   }
   TopkState& ts = e.ts;
   if (ts.active && dist <= ts.thr) {
+    ET_CHECK(ts.cnt < p.B && g < (uint32_t)p.n_groups);
     ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist), g);
     ++ts.cnt;
     if (mult >= (uint32_t)p.k) ts.thr = dist;   // one group alone bounds the k-th distance
@@ -1034,6 +1036,7 @@ __device__ __forceinline__ void dc_look(float (&v)[MT], const uint4& r, uint32_t
     // (bits 0..1 of a half-word are free; masked records keep no data there
     // either: & 0x7ffc is the offset)
     const uint32_t off = (((l & 1) ? (w[l >> 1] >> 16) : w[l >> 1]) & 0x7ffcu) ^ lane4;
+    ET_CHECK(off < 32768u);
     if (look & (1u << l)) v[l] = *smem_f32(off + (kDsmBase + ((uint32_t)(l - lv0) << 15)));
   }
 }
@@ -1246,6 +1249,7 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
 #pragma unroll
   for (int k = 0; k < NS; ++k) steps = max(steps, sl[k]);
   auto load_batch = [&](int k, uint32_t off) {
+    ET_CHECK(off + lane >= sl[k] || s0[k] + off + lane < (uint32_t)tr.n_leaves);
     return (off + lane < sl[k]) ? __ldg(rec + s0[k] + off + lane) : make_uint4(0u, 0u, 0u, 0u);
   };
   uint4 nx[NS];
@@ -1313,21 +1317,28 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
 #pragma unroll
           for (int k = 0; k < NS; ++k) dist[k] = dist[k] + v[k][l];
       }
+      if constexpr (!TOPK) {
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        const uint4 r = rr[k];
-        const uint32_t lf = s0[k] + off + j;
-        if constexpr (!TOPK) {
-          if (ok[k]) p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + lf] = dist[k];   // query-major rows
-        } else {
-          TopkState& ts = e.ts;
-          const uint32_t bucket = MASKED ? rec_mbucket_m<MT>(r) : rec_mbucket<MT>(r);
-          const bool em = ok[k] && ts.active && dist[k] <= ts.thr;
-          if (em) ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist[k]), lf);
-          ts.cnt += em ? 1 : 0;
-          ts.msum += em ? (1u << bucket) : 0u;
-          // one group alone (2^bucket <= multiplicity ids) bounds the k-th distance
-          if (em && (1u << bucket) >= (uint32_t)p.k) ts.thr = dist[k];
+        for (int k = 0; k < NS; ++k)
+          if (ok[k]) p.leafdist[((size_t)e.chunk * 32 + lane) * p.n_groups + s0[k] + off + j] = dist[k];
+      } else {
+        TopkState& ts = e.ts;
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) any |= ok[k] && dist[k] <= ts.thr;
+        if (__any_sync(FULLMASK, any && ts.active)) {   // warp-uniform: once thresholds are tight, rare
+#pragma unroll
+          for (int k = 0; k < NS; ++k) {
+            const uint4 r = rr[k];
+            const uint32_t bucket = MASKED ? rec_mbucket_m<MT>(r) : rec_mbucket<MT>(r);
+            const bool em = ok[k] && ts.active && dist[k] <= ts.thr;
+            ET_CHECK(!em || ts.cnt < p.B);
+            if (em) ts.buf[ts.cnt] = make_uint2(__float_as_uint(dist[k]), s0[k] + off + j);
+            ts.cnt += em ? 1 : 0;
+            ts.msum += em ? (1u << bucket) : 0u;
+            // one group alone (2^bucket <= multiplicity ids) bounds the k-th distance
+            if (em && (1u << bucket) >= (uint32_t)p.k) ts.thr = dist[k];
+          }
         }
       }
     }
@@ -1536,6 +1547,20 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     nq = __popc(__ballot_sync(FULLMASK, q >= 0));   // active lanes are a prefix
   }
   const int cell = p.chunk_cell ? __ldg(p.chunk_cell + chunk) : -1;
+  if (MODE != 1 && !p.chunk_lo) {
+    // the first record batch of each of this warp's streams into L1 now, so
+    // the scan does not start on an L2 round trip after the table build
+    const TreeDev& tr0 = p.tree[0];
+    const uint32_t len0 = (uint32_t)tr0.n_leaves;
+    const uint32_t a0 = (uint32_t)(((uint64_t)len0 * seg) / p.S), b0 = (uint32_t)(((uint64_t)len0 * (seg + 1)) / p.S);
+    const uint32_t wa0 = a0 + (uint32_t)(((uint64_t)(b0 - a0) * warp) / kWarps);
+    const uint32_t wb0 = a0 + (uint32_t)(((uint64_t)(b0 - a0) * (warp + 1)) / kWarps);
+#pragma unroll
+    for (int k = 0; k < kStreams; ++k) {
+      const uint32_t st0 = wa0 + (uint32_t)(((uint64_t)(wb0 - wa0) * k) / kStreams);
+      if (st0 + lane < wb0) asm volatile("prefetch.global.L1 [%0];" :: "l"(tr0.rec + st0 + lane));
+    }
+  }
   const float* lut0g = p.lut0 ? p.lut0 + (size_t)unit * kTmemLevels * 256 * 32 : nullptr;
 
   EmitCtx e;
