@@ -1547,20 +1547,6 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     nq = __popc(__ballot_sync(FULLMASK, q >= 0));   // active lanes are a prefix
   }
   const int cell = p.chunk_cell ? __ldg(p.chunk_cell + chunk) : -1;
-  if (MODE != 1 && !p.chunk_lo) {
-    // the first record batch of each of this warp's streams into L1 now, so
-    // the scan does not start on an L2 round trip after the table build
-    const TreeDev& tr0 = p.tree[0];
-    const uint32_t len0 = (uint32_t)tr0.n_leaves;
-    const uint32_t a0 = (uint32_t)(((uint64_t)len0 * seg) / p.S), b0 = (uint32_t)(((uint64_t)len0 * (seg + 1)) / p.S);
-    const uint32_t wa0 = a0 + (uint32_t)(((uint64_t)(b0 - a0) * warp) / kWarps);
-    const uint32_t wb0 = a0 + (uint32_t)(((uint64_t)(b0 - a0) * (warp + 1)) / kWarps);
-#pragma unroll
-    for (int k = 0; k < kStreams; ++k) {
-      const uint32_t st0 = wa0 + (uint32_t)(((uint64_t)(wb0 - wa0) * k) / kStreams);
-      if (st0 + lane < wb0) asm volatile("prefetch.global.L1 [%0];" :: "l"(tr0.rec + st0 + lane));
-    }
-  }
   const float* lut0g = p.lut0 ? p.lut0 + (size_t)unit * kTmemLevels * 256 * 32 : nullptr;
 
   EmitCtx e;
