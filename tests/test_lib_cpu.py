@@ -114,3 +114,15 @@ def test_fused_forest_scan_lookups(lib, seed, N, M, K, nd, split):
     assert all(g["scan_lookups"] == exp for g in got)
     t1 = api.et_build_stats(codes, K=K)[0]
     assert t1["scan_lookups"] == t1["lookups"]
+
+
+@pytest.mark.parametrize("split", [(0, 8), (0, 3, 8)])
+def test_byte_perm_stats_match_oracle_on_permuted_codes(lib, split):
+    """Encoding ordering (A21): building over a chunk permutation
+    equals building over the codes with their columns permuted first."""
+    codes = synth.random_codes(11, 4000, 8, 16, 300)
+    perm = np.random.default_rng(5).permutation(8).astype(np.int32)
+    got = api.et_build_stats(codes, split=list(split), K=16, byte_perm=perm)
+    ref = _oracle_stats(np.ascontiguousarray(codes[:, perm]), split)
+    for g, r in zip(got, ref):
+        assert (g["L1"], g["L2"], g["total_postfix"], g["lookups"]) == (r.L1, r.L2, r.total_postfix, r.lookups)
