@@ -286,9 +286,9 @@ static void upload_groups(et_index* ix, const Groups& g, const std::vector<uint3
 // (l, k = code byte l) inside that level's 32 KB shared-memory table,
 // (k << 7) | ((k & 31) << 2), so a lookup is one XOR with the lane's offset.
 // Levels 0 and 1 of an 8-level tree (held in TMEM) store the column k; half-
-// word 0 adds the LCP with the previous leaf in bits 8..11 and
-// floor(log2(multiplicity)) in bits 12..15; shorter trees keep both in
-// half-word 7 (bits 0..3, 4..7).
+// word 0 adds the lookup mask of the levels >= the LCP with the previous leaf
+// in bits 8..15 and half-word 1 floor(log2(multiplicity)) in bits 8..11;
+// shorter trees keep the LCP and the bucket in half-word 7 (bits 0..3, 4..7).
 static std::vector<uint4> make_records(const HostTree& h) {
   const int MT = h.MT;
   std::vector<uint4> rec(h.code.size());
@@ -302,7 +302,10 @@ static std::vector<uint4> make_records(const HostTree& h) {
     const uint64_t mu = (i < h.mult.size()) ? h.mult[i] : 1;
     uint32_t mb = 0;   // floor(log2(multiplicity)), capped at 15
     while (mb < 15 && (2ull << mb) <= mu) ++mb;
-    if (MT == 8) w[0] |= (lcp << 8) | (mb << 12);
+    // 8-level trees: the lookup mask (levels >= LCP) in half-word 0 bits
+    // 8..15 and the bucket in half-word 1 bits 8..11 -- the fused-forest
+    // record layout, so one scan loop serves both
+    if (MT == 8) { w[0] |= ((0xffu << lcp) & 0xffu) << 8; w[1] |= mb << 8; }
     else w[7] = lcp | (mb << 4);
     rec[i] = make_uint4(w[0] | (w[1] << 16), w[2] | (w[3] << 16), w[4] | (w[5] << 16), w[6] | (w[7] << 16));
   }
@@ -724,6 +727,7 @@ struct Carve {
 };
 
 struct Work {
+  float4* cbt;   // chunk-major codebook copy for the wide table build (s > 16)
   float* luts;
   int* chunk_q; int* qslot_off; int* qslot;
   float* lut0; float* partials; float* leafdist;
@@ -733,6 +737,8 @@ struct Work {
 
 static Work carve(Carve& c, const et_index* ix, const Plan& pl, int64_t Q, bool full, int slots_per_q) {
   Work w{};
+  // (s is a per-call argument: room for s <= 64, i.e. K * M * 16 float4)
+  w.cbt = (pl.MTmax == 8) ? c.take<float4>((size_t)ix->K * ix->M * 16) : nullptr;
   w.luts = pl.mat_luts ? c.take<float>((size_t)Q * ix->M * ix->K) : nullptr;
   w.chunk_q = c.take<int>((size_t)pl.n_chunks * 32);
   w.qslot_off = c.take<int>(Q + 1);
@@ -783,6 +789,8 @@ static size_t ivf_ws_bytes(const et_index* ix, const Plan& pl, int64_t Q, int w)
 
 static void fill_scan_common(ScanParams& sp, const et_index* ix, const Plan& pl) {
   sp.M = ix->M; sp.K = ix->K;
+  static const int wide_old = [] { const char* e = std::getenv("ET_WIDE_OLD"); return e && e[0] == '1'; }();
+  sp.wide_old = wide_old;
   sp.layer_sub = ix->layer_sub_d.as<int>();
   for (int l = 0; l < ix->M && l < kMaxTrees * kMaxMT; ++l) sp.lsub[l] = ix->layer_sub[l];
   if (ix->fused) {   // the forest's tuples scanned as one masked tree over all M levels
@@ -831,6 +839,15 @@ static void table_source(ScanParams& sp, const et_index* ix, const float* codebo
     sp.s = d / ix->M;
     sp.vec4 = aligned16(queries) && aligned16(codebooks) && (d % 4 == 0) ? 1 : 0;
   }
+}
+
+// Fused tables with 16 < s <= 64 (c3): the chunk-major codebook copy the wide
+// build reads (layout only; one small kernel per call).
+static void chunk_codebook(ScanParams& sp, const et_index* ix, const Work& w, cudaStream_t st) {
+  if (sp.luts || !w.cbt || !sp.vec4 || sp.s <= 16 || sp.s > 64 || sp.s % 4) return;
+  cuda_check(timed("cb_chunks", st, [&] { return launch_cb_chunks(sp.codebooks, ix->M, ix->K, sp.s, w.cbt, st); }),
+             "cb_chunks");
+  sp.cbt = w.cbt;
 }
 
 // Materialised-tables plan: lut_kernel writes [Q][M][K] into the workspace
@@ -1014,6 +1031,7 @@ et_status et_etree_distances(const et_index* ix, const float* codebooks, int32_t
   cudaStream_t st = (cudaStream_t)stream;
   cuda_check(timed("fill", st, [&] { return launch_fill_flat(Q, pl.n_chunks, w.chunk_q, w.qslot_off, w.qslot, st); }), "fill");
   materialise(sp, ix, pl, w, Q, st);
+  chunk_codebook(sp, ix, w, st);
   fill_scan_common(sp, ix, pl);
   sp.chunk_q = w.chunk_q;
   sp.lut0 = w.lut0;
@@ -1046,6 +1064,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   Work w = carve(c, ix, pl, Q, false, 1);
   cudaStream_t st = (cudaStream_t)stream;
   materialise(sp, ix, pl, w, Q, st);
+  chunk_codebook(sp, ix, w, st);
   fill_scan_common(sp, ix, pl);
   sp.flatQ = Q;   // arithmetic chunking: no fill launch
   sp.lut0 = w.lut0;

@@ -66,6 +66,7 @@ struct ScanParams {
   const float* codebooks = nullptr;   // [M][K][s]        (fused tables)
   const float* queries = nullptr;     // [Q][d]           (fused tables)
   const float* luts = nullptr;        // [Q][M][K]        (materialised tables) or null
+  const float4* cbt = nullptr;        // [M][s/4][K] chunk-major codebook copy (16 < s <= 64) or null
   const float* coarse = nullptr;      // [nlist][d]       (IVF residual tables) or null
   const int* layer_sub = nullptr;     // [M] subspace of each code byte (chunk order), device copy
   int lsub[kMaxTrees * kMaxMT] = {};  // the same, by value (kernel parameters: no dependent load)
@@ -104,6 +105,7 @@ struct ScanParams {
   int qthr_shared = 0;                // several units per query (S > 1, IVF): share during the scan
   int vec4 = 1;                       // query/codebook rows 16-byte aligned
   int compact = 0;                    // merge each lane's 16 per-warp lists at the end (long lists)
+  int wide_old = 0;                   // experiments (ET_WIDE_OLD=1): s > 16 8-level trees use build_tables_wide
   // ---- fused E-Forest (M <= 8) ----
   int masked = 0;                     // records carry a per-level lookup mask (fused forest tuple records)
   uint32_t fsplit = 0;                // bit l set: level l starts a forest tree (partials summed in tree order)
@@ -137,6 +139,7 @@ cudaError_t launch_fill_flat(int64_t Q, int n_chunks, int* chunk_q, int* qslot_o
 cudaError_t launch_gather_full(const float* leafdist, const uint32_t* slot2group,
                                int64_t n_groups, int64_t n, const int* qslot, int64_t Q,
                                float* out, cudaStream_t st);
+cudaError_t launch_cb_chunks(const float* codebooks, int M, int K, int s, float4* out, cudaStream_t st);
 cudaError_t launch_luts(const float* codebooks, int d, int M, int K, const float* queries,
                         int64_t Q, float* luts, bool vec4, cudaStream_t st);
 cudaError_t launch_flat_adc(const float* luts, int64_t Q, int M, int K, const uint8_t* codes,

@@ -4,6 +4,8 @@
 #pragma once
 #include "common.cuh"
 
+#include <type_traits>
+
 namespace et {
 namespace {   // internal linkage: every scan_s*.cu has its own copy
 
@@ -665,6 +667,158 @@ __device__ void build_tables_wide(const ScanParams& p, const SmemScan& sm, int t
   }
 }
 
+// Table build of an 8-level tree with long sub-vectors (16 < s <= 64, s % 4 ==
+// 0; c3: s = 60) for at most 8 queries, organised like build_tables_resident8:
+// the queries' sub-vectors of all 8 levels are staged once as query pairs
+// [level][pair][dim][2] in the staging area (8 x 4 x s x 8 B <= 16 KB), four
+// levels are built at a time by kWPL warps each, a lane owns kR codeword rows
+// and keeps its 4 x kR x pairs packed accumulators in registers over the whole
+// j-ascending chain while the codeword rows stream through registers 4
+// dimensions at a time (next chunk in flight).  Every broadcast LDS.128 of a
+// staged pair (2 queries x 2 dims) feeds 4 kR packed FADD2/FFMA2.  Levels 0/1
+// are built into regions 2/3 and copied to TMEM before round 1, exactly as in
+// the resident build, so the scan sees the same layout.
+template <int SS>
+struct Wide8 {
+  static_assert(SS > kDC && SS <= 64 && SS % 4 == 0, "wide resident build: 16 < s <= 64, s % 4 == 0");
+  static constexpr int NP = 4;                            // query pairs (nq <= 8)
+  static constexpr uint32_t pair_bytes = SS * 8u;         // [dim][2] fp32
+  static constexpr uint32_t lvl_bytes = NP * pair_bytes;
+  static constexpr int NCH = SS / 4;                      // 4-dimension codeword chunks
+  static_assert(8 * lvl_bytes <= 8u * 16u * 128u, "staging area");
+};
+
+// Stage tree t's query sub-vectors for build_tables_wide8: plain E-Tree
+// tables are copied with cp.async (issued early -- at kernel entry, or while
+// the previous tree is scanned -- and awaited by the build); IVF residuals
+// (x - cc) synchronously.
+template <int SS>
+__device__ __forceinline__ void stage_wide8(const ScanParams& p, const SmemScan& sm, int t, int nq, int cell) {
+  using W = Wide8<SS>;
+  const TreeDev& tr = p.tree[t];
+  const uint32_t stg_s = smem_u32(sm.bigstage);
+  for (int e = threadIdx.x; e < 8 * 8 * SS; e += kThreads) {   // (level, slot, dim)
+    const int l = e / (8 * SS), r = e - l * (8 * SS);
+    const int i = r / SS, j = r - i * SS;
+    if (i >= nq) continue;                                // slots >= nq: never looked up
+    const int m = p.lsub[tr.layer0 + l];
+    const float* src = p.queries + (size_t)sm.qidx[i] * p.d + (size_t)m * SS + j;
+    const uint32_t dst = stg_s + (uint32_t)l * W::lvl_bytes + (uint32_t)(i >> 1) * W::pair_bytes + (uint32_t)j * 8u +
+                         (uint32_t)(i & 1) * 4u;
+    if (cell >= 0 && p.coarse) sts(dst, __ldg(src) - __ldg(p.coarse + (size_t)cell * p.d + (size_t)m * SS + j));
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+  }
+}
+
+// Table build of an 8-level tree with long sub-vectors (16 < s <= 64, s % 4 ==
+// 0; c3: s = 60) for at most 8 queries, organised like build_tables_resident8:
+// the queries' sub-vectors of all 8 levels are staged once as query pairs
+// [level][pair][dim][2] in the staging area (stage_wide8), four levels are
+// built at a time by kWPL warps each, a lane owns kR codeword rows and keeps
+// its kR x pairs packed accumulators in registers over the whole j-ascending
+// chain while the codeword rows stream through registers 4 dimensions at a
+// time (two chunks in flight).  Codeword chunks come from the chunk-major copy
+// p.cbt [m][s/4][K] float4 (one coalesced 512 B load per warp and row block;
+// the row-major codebook would touch 32 rows per load instruction), else from
+// the rows.  Every broadcast LDS.128 of a staged pair (2 queries x 2 dims)
+// feeds 2 kR packed FADD2/FFMA2.  Levels 0/1 are built into regions 2/3 and
+// copied to TMEM before round 1, exactly as in the resident build.
+template <int SS>
+__device__ void build_tables_wide8(const ScanParams& p, const SmemScan& sm, int t, int nq) {
+  using W = Wide8<SS>;
+  constexpr int NP = W::NP, NCH = W::NCH;
+  const TreeDev& tr = p.tree[t];
+  const int K = p.K;
+  const int lane = lane_id(), warp = warp_id();
+  const uint32_t dsm_s = smem_u32(et_dsm);
+  const uint32_t tab_s = smem_u32(sm.tab);
+  const uint32_t stg_s = smem_u32(sm.bigstage);
+  (void)nq;
+  const int lw = warp / kWPL;                             // level within the round
+  const int row0 = (warp % kWPL) * 32 * kR;               // first codeword row of this warp
+  const bool active = row0 < K;
+  // codeword chunks of level l stream through a register ring, kRing - 1
+  // chunks ahead (the L2 latency is longer than one chunk's arithmetic); the
+  // ring of the next level is filled before each barrier / copy
+  constexpr int kRing = 5;
+  float4 c[kRing][kR];
+  auto chunk = [&](int l, int r, int jc) -> float4 {
+    const int m = p.lsub[tr.layer0 + l];
+    const int k = min(row0 + 32 * r + lane, K - 1);
+    if (p.cbt) return __ldg(p.cbt + ((size_t)m * NCH + jc) * K + k);
+    return __ldg(reinterpret_cast<const float4*>(p.codebooks + ((size_t)m * K + k) * SS) + jc);
+  };
+  auto prefill = [&](int l) {
+#pragma unroll
+    for (int d = 0; d < kRing - 1; ++d)
+#pragma unroll
+      for (int r = 0; r < kR; ++r)
+        if (d < NCH) c[d][r] = chunk(l, r, d);
+  };
+  if (active) prefill(lw);
+  asm volatile("cp.async.wait_all;" ::: "memory");         // this thread's staged copies landed
+  __syncthreads();                                        // everyone's; previous users of the tables done
+  auto item = [&](uint32_t dst_s, int l) {
+    const uint32_t xs = stg_s - dsm_s + (uint32_t)l * W::lvl_bytes;
+    unsigned long long a[NP][kR];
+#pragma unroll
+    for (int pi = 0; pi < NP; ++pi)
+#pragma unroll
+      for (int r = 0; r < kR; ++r) a[pi][r] = 0ull;
+#pragma unroll
+    for (int jc = 0; jc < NCH; ++jc) {
+      if (jc + kRing - 1 < NCH) {
+#pragma unroll
+        for (int r = 0; r < kR; ++r) c[(jc + kRing - 1) % kRing][r] = chunk(l, r, jc + kRing - 1);
+      }
+      const int cs = jc % kRing;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {                       // dims 4 jc + 2 h, 4 jc + 2 h + 1
+        // every pair, branch-free (slots >= nq hold stale stage data: their
+        // entries are computed and stored but never looked up)
+#pragma unroll
+        for (int pi = 0; pi < NP; ++pi) {
+          const float4 u = lds4_off(xs + (uint32_t)pi * W::pair_bytes + (uint32_t)(4 * jc + 2 * h) * 8u);
+          const unsigned long long p0 = f2pack(u.x, u.y), p1 = f2pack(u.z, u.w);
+#pragma unroll
+          for (int r = 0; r < kR; ++r) {
+            const float c0 = h ? c[cs][r].z : c[cs][r].x, c1 = h ? c[cs][r].w : c[cs][r].y;
+            a[pi][r] = f2sqacc(f2subs(p0, c0), a[pi][r]);
+            a[pi][r] = f2sqacc(f2subs(p1, c1), a[pi][r]);
+          }
+        }
+      }
+    }
+    const uint32_t rows = dst_s - dsm_s + ((uint32_t)(row0 + lane) << 7);
+    const uint32_t sw = (uint32_t)(row0 + lane) << 2;
+#pragma unroll
+    for (int pi = 0; pi < NP; ++pi) {
+      const uint32_t i4 = (uint32_t)pi * 8u;
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        float e0, e1;
+        f2unpack(a[pi][r], e0, e1);
+        const uint32_t row = rows + ((uint32_t)r << 12);
+        sts_off(row + ((i4 ^ sw) & 0x7cu), e0);
+        sts_off(row + (((i4 + 4) ^ sw) & 0x7cu), e1);
+      }
+    }
+  };
+  // round 0: level lw -> region (levels 0, 1: regions 2, 3 until the TMEM copy)
+  const uint32_t r0 = (lw < 2) ? (uint32_t)(lw + 2) : (uint32_t)(lw - 2);
+  if (active) item(tab_s + (r0 << 15), lw);
+  if (active) prefill(lw + 4);                            // round 1's first chunks, in flight during the copy
+  __syncthreads();
+  tmem_fence_after();
+  tmem_load_from_smem(sm, tab_s + (2u << 15), tab_s + (3u << 15));
+  tmem_fence_before();
+  __syncthreads();                                        // regions 2, 3 free again
+  // round 1: level lw + 4 -> region lw + 2
+  if (active) item(tab_s + ((uint32_t)(lw + 2) << 15), lw + 4);
+  __syncthreads();                                        // tables complete; the stage is free
+  tmem_fence_after();
+}
+
 // Build the tables of tree t for this CTA's queries (fused).
 // Passes over (level, 16-dimension chunk): the chunk of the active queries'
 // sub-vectors (minus the coarse centroid for IVF residuals) is staged in shared
@@ -960,16 +1114,19 @@ __device__ __forceinline__ const float* smem_f32(uint32_t a) {
 }
 
 
+// Levels a leaf looks up (bit l: l >= its LCP with the previous leaf): 8-level
+// records store the mask (half-word 0 bits 8..15, one byte extract), shorter
+// trees the LCP (half-word 7 bits 0..3).
 template <int MT>
-__device__ __forceinline__ uint32_t rec_lcp(const uint4& r) {
-  if constexpr (MT == 8) return (r.x >> 8) & 15u;
-  else return (r.w >> 16) & 15u;
+__device__ __forceinline__ uint32_t rec_look(const uint4& r) {
+  if constexpr (MT == 8) return __byte_perm(r.x, 0u, 0x4441);
+  else return (0xffu << ((r.w >> 16) & 15u)) & ((1u << MT) - 1u);
 }
 // floor(log2(multiplicity)) of the leaf's group (single trees), capped at 15:
 // 2^bucket >= k proves the group alone holds k ids (a conservative test)
 template <int MT>
 __device__ __forceinline__ uint32_t rec_mbucket(const uint4& r) {
-  if constexpr (MT == 8) return (r.x >> 12) & 15u;
+  if constexpr (MT == 8) return (r.x >> 24) & 15u;
   else return (r.w >> 20) & 15u;
 }
 
@@ -985,9 +1142,12 @@ __device__ __forceinline__ uint32_t rec_mbucket(const uint4& r) {
 // The TMEM levels' entries of a record (levels 0 and 1 of an 8-level tree:
 // columns k0 and 256 + k1): issued without waiting; the caller waits once
 // for every stream's reads (tmem_wait_all) before dc_leaf uses them.
+// The address is one byte permute: the column byte of the record under the
+// quadrant's lane base (tq's column bits are 0: the CTA allocates all 512
+// columns), level 1 at column offset 256.
 __device__ __forceinline__ void tmem_rec_ld(uint32_t tq, const uint4& r, uint32_t& t0, uint32_t& t1) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(t0) : "r"(tq + (r.x & 255u)));
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(t1) : "r"(tq + 256u + ((r.x >> 16) & 255u)));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(t0) : "r"(__byte_perm(r.x, tq, 0x7650)));
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(t1) : "r"(__byte_perm(r.x, tq, 0x7652) + 256u));
 }
 template <int NS>
 __device__ __forceinline__ void tmem_wait_all(uint32_t (&t0)[NS], uint32_t (&t1)[NS]) {
@@ -1028,33 +1188,35 @@ __device__ __forceinline__ void dc_look(float (&v)[MT], const uint4& r, uint32_t
   constexpr int lv0 = lv0_of(MT);
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
   if constexpr (lv0 == 2) {
-    if (look & 1u) v[0] = __uint_as_float(t0);
-    if (look & 2u) v[1] = __uint_as_float(t1);
+    // the TMEM levels are read for every leaf: a level outside `look` holds
+    // the byte of the previous leaf (shared prefix / unchanged tree bytes), so
+    // the read returned the very entry v already holds -- no select needed
+    (void)look;
+    v[0] = __uint_as_float(t0);
+    v[1] = __uint_as_float(t1);
   }
 #pragma unroll
   for (int l = lv0; l < MT; ++l) {
-    // (bits 0..1 of a half-word are free; masked records keep no data there
-    // either: & 0x7ffc is the offset)
-    const uint32_t off = (((l & 1) ? (w[l >> 1] >> 16) : w[l >> 1]) & 0x7ffcu) ^ lane4;
+    // shared-memory half-words are pure offsets (< 32768; the LCP / mask /
+    // bucket fields live in the TMEM half-words or in unused level 7)
+    const uint32_t off = ((l & 1) ? (w[l >> 1] >> 16) : (w[l >> 1] & 0xffffu)) ^ lane4;
     ET_CHECK(off < 32768u);
     if (look & (1u << l)) v[l] = *smem_f32(off + (kDsmBase + ((uint32_t)(l - lv0) << 15)));
   }
 }
 
 template <int MT>
-__device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t pl, bool valid,
+__device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_t look,
                                          uint32_t lane4, uint32_t t0, uint32_t t1) {
   constexpr int lv0 = lv0_of(MT);
   const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-  // levels looked up: l >= LCP, as a bit mask (the compiler turns the tests
-  // below into one R2P instead of a compare per level)
-  const uint32_t look = valid ? ((0xffu << pl) & 0xffu) : 0u;
+  // look: levels looked up (l >= LCP) as a bit mask (the compiler turns the
+  // tests below into one R2P instead of a compare per level)
   if constexpr (lv0 == 2) {
     // levels 0 and 1 (TMEM, columns k0 and 256 + k1, read by the caller: t0,
-    // t1) take effect only on a new subtree at depth 0 / <= 1 -- otherwise
-    // the read returned the very entry the path already holds
-    if (look & 1u) v[0] = __uint_as_float(t0);
-    if (look & 2u) v[1] = __uint_as_float(t1);
+    // t1): outside `look` the read returned the very entry the path holds
+    v[0] = __uint_as_float(t0);
+    v[1] = __uint_as_float(t1);
   }
 #pragma unroll
   for (int l = lv0; l < MT; ++l) {
@@ -1079,7 +1241,7 @@ __device__ __forceinline__ float dc_leaf(float (&v)[MT], const uint4& r, uint32_
 // = mask | bucket << 8.
 template <int MT>
 __device__ __forceinline__ uint32_t rec_mask(const uint4& r) {
-  if constexpr (MT == 8) return (r.x >> 8) & 255u;
+  if constexpr (MT == 8) return __byte_perm(r.x, 0u, 0x4441);
   else return (r.w >> 16) & 255u;
 }
 template <int MT>
@@ -1088,42 +1250,6 @@ __device__ __forceinline__ uint32_t rec_mbucket_m(const uint4& r) {
   else return (r.w >> 24) & 15u;
 }
 
-// dc_leaf for masked records: level l is looked up iff bit l of `mask`
-// (warp-uniform); the distance is summed per forest tree left to right and
-// the per-tree partials in tree order, ((p_0 + p_1) + ...) (reading A13):
-// bit l of `fsplit` marks the first level of tree u >= 1.
-template <int MT, int FS>
-__device__ __forceinline__ float dc_leaf_m(float (&v)[MT], const uint4& r, uint32_t mask, uint32_t lane4,
-                                           uint32_t t0, uint32_t t1, uint32_t fsplit) {
-  constexpr int lv0 = lv0_of(MT);
-  const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-  if constexpr (lv0 == 2) {   // TMEM levels read by the caller (t0, t1)
-    if (mask & 1u) v[0] = __uint_as_float(t0);
-    if (mask & 2u) v[1] = __uint_as_float(t1);
-  }
-#pragma unroll
-  for (int l = lv0; l < MT; ++l) {
-    const uint32_t off = (((l & 1) ? (w[l >> 1] >> 16) : w[l >> 1]) & 0x7ffcu) ^ lane4;
-    if (mask & (1u << l)) v[l] = *smem_f32(off + (kDsmBase + ((uint32_t)(l - lv0) << 15)));
-  }
-  if constexpr (FS > 0 && FS < MT) {   // two trees split at level FS (compile time): p_0 + p_1
-    float s0 = v[0], s1 = v[FS];
-#pragma unroll
-    for (int l = 1; l < FS; ++l) s0 = s0 + v[l];
-#pragma unroll
-    for (int l = FS + 1; l < MT; ++l) s1 = s1 + v[l];
-    return s0 + s1;
-  } else {
-    float tot = 0.f, s = v[0];
-    bool have = false;
-#pragma unroll
-    for (int l = 1; l < MT; ++l) {
-      if ((fsplit >> l) & 1u) { tot = have ? tot + s : s; have = true; s = v[l]; }
-      else s = s + v[l];
-    }
-    return have ? tot + s : s;
-  }
-}
 
 // Scan of leaves [a, b) of one tree by one warp, lane = query.  The range is
 // split into two halves scanned in lockstep (two independent dependency
@@ -1195,16 +1321,17 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
         const uint4 r0 = shfl_rec(mine0, j), r1 = shfl_rec(mine1, j);
         const uint32_t leaf0 = a + off + j, leaf1 = m + off + j;
         const bool ok1 = j < n1;
-        const uint32_t pl0 = (off + j == 0) ? 0u : rec_lcp<MT>(r0);   // range starts: rebuild the path
-        const uint32_t pl1 = (off + j == 0) ? 0u : rec_lcp<MT>(r1);
+        constexpr uint32_t kAll = (1u << MT) - 1u;
+        const uint32_t lk0 = (off + j == 0) ? kAll : rec_look<MT>(r0);   // range starts: rebuild the path
+        const uint32_t lk1 = ok1 ? ((off + j == 0) ? kAll : rec_look<MT>(r1)) : 0u;
         uint32_t t0[2] = {0u, 0u}, t1[2] = {0u, 0u};
         if constexpr (lv0_of(MT) == 2) {
           tmem_rec_ld(tq, r0, t0[0], t1[0]);
           tmem_rec_ld(tq, r1, t0[1], t1[1]);
           tmem_wait_all<2>(t0, t1);
         }
-        const float d0 = dc_leaf<MT>(v0, r0, pl0, true, lane4, t0[0], t1[0]);
-        const float d1 = dc_leaf<MT>(v1, r1, pl1, ok1, lane4, t0[1], t1[1]);
+        const float d0 = dc_leaf<MT>(v0, r0, lk0, lane4, t0[0], t1[0]);
+        const float d1 = dc_leaf<MT>(v1, r1, lk1, lane4, t0[1], t1[1]);
         emit(leaf0, d0, r0, true);
         emit(leaf1, d1, r1, ok1);
       }
@@ -1268,8 +1395,13 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
       nx[k] = load_batch(k, off + 32);
     }
     const int n = (int)min(32u, steps - off);
-    for (int j = 0; j < n; ++j) {
-      const bool first = (off + j == 0);             // range start: rebuild the path
+    // Generic steps (the range's first leaf: every level looked up; the last
+    // step: the shorter streams are done) test per stream; all other steps
+    // run a copy of the body with those tests compiled out.
+    auto step = [&](int j, auto gen_tag) {
+      constexpr bool GEN = decltype(gen_tag)::value;
+      // range start: rebuild the path (generic steps only)
+      const uint32_t fm = GEN ? ((off + j == 0) ? kAll : 0u) : 0u;
       uint4 rr[NS];
       uint32_t t0[NS], t1[NS];                       // TMEM levels: every stream's reads, one wait
 #pragma unroll
@@ -1284,10 +1416,10 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
       bool ok[NS];
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        ok[k] = off + j < sl[k];
+        ok[k] = GEN ? (off + j < sl[k]) : true;   // fast steps: every stream has this leaf
         uint32_t look;
-        if constexpr (MASKED) look = ok[k] ? (first ? kAll : rec_mask<MT>(rr[k])) : 0u;
-        else look = ok[k] ? ((0xffu << (first ? 0u : rec_lcp<MT>(rr[k]))) & kAll) : 0u;
+        if constexpr (MASKED) look = ok[k] ? (rec_mask<MT>(rr[k]) | fm) : 0u;
+        else look = ok[k] ? (rec_look<MT>(rr[k]) | fm) : 0u;
         dc_look<MT>(v[k], rr[k], look, lane4, t0[k], t1[k]);
       }
       float dist[NS];
@@ -1341,6 +1473,13 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
           }
         }
       }
+    };
+    for (int j = 0; j < n; ++j) {
+      // (fast copies for the top-k scans of single trees and two-tree fused
+      // forests; ptxas 12.9 runs out of predicate registers on the others)
+      constexpr bool kFast = TOPK && (!MASKED || (FS > 0 && FS < MT));
+      if (!kFast || off + j == 0 || off + j + 1 >= steps) step(j, std::true_type{});
+      else step(j, std::false_type{});
     }
     if constexpr (TOPK) {   // prune full buffers; share the threshold with the CTA's other warps
       refresh_if_needed(e);  // and with every other unit scanning the same query
@@ -1567,6 +1706,14 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     e.ts.buf = e.ts.warp_buf + (size_t)lane * kWarps * p.B;
   }
 
+  if constexpr (!(SS == kDC && MTC > 0)) phase_mark(unit, 1);
+  // s > 16 trees of 8 levels for <= 8 queries: the wide resident build
+  auto wide8 = [&](int tt) {
+    if constexpr (SS > kDC && SS <= 64 && SS % 4 == 0)
+      return nq <= 8 && !p.luts && p.vec4 && p.tree[tt].MT == 8 && use_tmem && !p.wide_old;
+    else
+      return false;
+  };
   // Forest: trees T-1..1 first (per-leaf partials for this CTA's queries),
   // then tree 0, whose leaves walk their tuples and sum in tree order.
   for (int t = p.T - 1; t >= 0; --t) {
@@ -1582,7 +1729,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       }
     } else {
       if constexpr (SS > kDC && SS <= 64 && SS % 4 == 0) {
-        if (nq <= 8 && !p.luts && p.vec4) build_tables_wide<SS>(p, sm, t, unit, nq, cell);
+        if (wide8(t)) {
+          if (t == p.T - 1) stage_wide8<SS>(p, sm, t, nq, cell);   // (later trees: staged during the previous scan)
+          build_tables_wide8<SS>(p, sm, t, nq);
+          level0_done = true;
+          if (t > 0 && wide8(t - 1)) stage_wide8<SS>(p, sm, t - 1, nq, cell);   // lands while tree t is scanned
+        } else if (nq <= 8 && !p.luts && p.vec4) build_tables_wide<SS>(p, sm, t, unit, nq, cell);
         else build_tables<SS>(p, sm, t, unit, nq, cell);
       } else {
         build_tables<SS>(p, sm, t, unit, nq, cell);
@@ -1596,6 +1748,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       __syncthreads();
       tmem_fence_after();
     }
+    if constexpr (!(SS == kDC && MTC > 0)) phase_mark(unit, t == 0 ? 7 : 5);   // tables of tree t ready
     uint32_t lo = 0, hi = (uint32_t)tr.n_leaves;
     if (t == 0) {
       if (p.chunk_lo) { lo = __ldg(p.chunk_lo + chunk); hi = __ldg(p.chunk_hi + chunk); }
@@ -1620,6 +1773,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
     tmem_fence_before();
     __syncthreads();   // partials visible / tables free for the next tree
     tmem_fence_after();
+    if constexpr (!(SS == kDC && MTC > 0)) phase_mark(unit, t == 0 ? 2 : 6);   // tree t scanned
   }
   if constexpr (FOREST) {   // the CTA's warps split the tuples evenly
     const uint64_t G = (uint64_t)p.n_groups;

@@ -5,3 +5,10 @@
 namespace et {
 cudaError_t launch_scan_60(const ScanParams& p, size_t smem, cudaStream_t st) { return launch_scan_s<60>(p, smem, st); }
 }  // namespace et
+
+#ifdef ET_PHASE_TIMING
+extern "C" int et_debug_phases_s60(unsigned long long* out, int n_units) {
+  if (n_units > (1 << 16)) n_units = 1 << 16;
+  return (int)cudaMemcpyFromSymbol(out, et::g_phase, (size_t)n_units * 8 * sizeof(unsigned long long));
+}
+#endif

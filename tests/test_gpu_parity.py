@@ -239,6 +239,19 @@ def test_forest_c3_shape_topk_and_full(c3s):
     check_topk(d.cpu().numpy(), i.cpu().numpy(), cb, qx, codes, 100, range(cfg.Q))
     ref = pq.adc(pq.lut64(cb, qx), codes)
     assert rel_err(full.cpu().numpy(), ref).max() <= RTOL
+    # tables built inside the scan CTAs (s = 60 wide build) == lut_kernel's
+    # materialised tables, bit for bit: the same j-ascending FMA chains
+    luts = api.et_compute_luts(dev(cb), dev(qx))
+    full_m = ix.et_etree_distances(luts=luts)
+    torch.cuda.synchronize()
+    assert torch.equal(full, full_m)
+    # chunk sizes 1..8 queries per CTA (odd and even pair counts): 1181 queries
+    # over the SMs; fused top-k == materialised top-k exactly
+    qb = np.concatenate([qx] * 25)[:1181]
+    df, if_ = ix.et_etree_topk(100, queries=dev(qb), codebooks=dev(cb))
+    dm, im = ix.et_etree_topk(100, luts=api.et_compute_luts(dev(cb), dev(qb)))
+    torch.cuda.synchronize()
+    assert torch.equal(df, dm) and torch.equal(if_, im)
 
 
 def test_forest_T1_equals_tree_and_split_invariance(c1):

@@ -2,7 +2,8 @@
 
   python tools/phase_timing.py --config c2
 Phases: 0 start, 1 build start, 5 staged, 6 round 0 built (levels 0-3), 7 TMEM levels copied,
-2 build done, 3 scan done, 4 compaction done.
+2 build done, 3 scan done, 4 compaction done.  s = 60 joined forests (c3): 1 setup done,
+5/6 tree 1 tables/scan, 7/2 tree 0 tables/scan, 3 join done, 4 end.
 """
 import argparse
 import ctypes as C
@@ -38,13 +39,18 @@ def main():
     lib = api._lib.load()
     n = 1 << 16
     buf = np.zeros((n, 8), dtype=np.uint64)
-    lib.et_debug_phases.argtypes = [C.c_void_p, C.c_int]
-    lib.et_debug_phases(buf.ctypes.data, n)
+    s60 = cfg.d // cfg.M == 60
+    fn = lib.et_debug_phases_s60 if s60 else lib.et_debug_phases
+    fn.argtypes = [C.c_void_p, C.c_int]
+    fn(buf.ctypes.data, n)
     used = buf[:, 0] > 0
     b = buf[used].astype(np.float64)
     t0 = b[:, 0].min()
     order = [(0, 1, "start->build"), (1, 5, "stage"), (5, 6, "round 0"), (6, 7, "TMEM copy"),
              (7, 2, "round 1"), (2, 3, "scan"), (3, 4, "compaction")]
+    if s60:   # joined forest (T = 2): tree 1 tables, tree 1 scan, tree 0 tables, tree 0 scan, join
+        order = [(0, 1, "setup"), (1, 5, "tables tree 1"), (5, 6, "scan tree 1"), (6, 7, "tables tree 0"),
+                 (7, 2, "scan tree 0"), (2, 3, "join"), (3, 4, "tail")]
     print(f"units {used.sum()}  kernel span {(b[:, 4].max() - t0) / 1e3:.1f} us")
     for i, j, name in order:
         d = (b[:, j] - b[:, i]) / 1e3
