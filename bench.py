@@ -937,6 +937,10 @@ def run_ours(args):
         if os.path.exists(tr):
             with open(tr) as f:
                 roof["traffic"] = json.load(f).get(args.config, {}).get("scan")
+        try:   # launch plan (chunks of <= 32 queries, leaf segments, streams per warp)
+            plan_info = None if ivf else ix.et_plan_info(Ql, 0 if full else kk)
+        except Exception:   # noqa: BLE001  (an older library without et_plan_info)
+            plan_info = None
         wl = (f"{cfg.name}: BASELINE configs[{CFG_INDEX[cfg.name]}]" if cfg.name in CFG_INDEX
               else f"{cfg.name}: diagnostic companion")
         par = {"none": "1 GPU",
@@ -953,6 +957,7 @@ def run_ours(args):
                        "forest_split": cfg.forest_split, "parallelism": par, "shard_mode": mode,
                        "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
                        "index_build_s": round(build_s, 3),
+                       "plan": plan_info,
                        "timing": ("CUDA graph replay of one step, CUDA events per step" if world == 1
                                   else "CUDA events per step, max over ranks")},
             "roofline": roof,

@@ -171,6 +171,14 @@ et_status et_compute_luts(const float* codebooks, int32_t d, int32_t M, int32_t 
 et_status et_workspace_size(const et_index* index, int64_t Q, int32_t k,
                             int32_t nprobe, size_t* bytes);
 
+/* The launch plan et_etree_topk (k > 0) or et_etree_distances (k <= 0) uses
+ * for Q queries on the current device: query chunks (one CTA each, <= 32
+ * queries), leaf segments per chunk (S) and lockstep leaf streams per scan
+ * warp.  Host only (no launch).  Errors: ET_ERR_CONFIG (null argument, Q < 1,
+ * IVF index: its chunks depend on the probes). */
+et_status et_plan_info(const et_index* index, int64_t Q, int32_t k, int32_t* n_chunks,
+                       int32_t* S, int32_t* streams);
+
 /* Full output: out[q][slot] = ADC distance of database slot for
  * query q, [Q][n].  Either `luts` ([Q][M][K]) or `queries` ([Q][d]) + the
  * codebooks the index was built against must be given (queries => the tables

@@ -155,6 +155,12 @@ class Index:
     def stats(self):
         return [self.et_index_stats(t) for t in range(self.T)]
 
+    def et_plan_info(self, Q: int, k: int) -> dict:
+        """The launch plan of et_etree_topk (k > 0) / et_etree_distances (k <= 0)."""
+        c, s, ns = C.c_int32(), C.c_int32(), C.c_int32()
+        check(_lib.load().et_plan_info(self._h, Q, k, C.byref(c), C.byref(s), C.byref(ns)))
+        return {"chunks": c.value, "S": s.value, "streams": ns.value}
+
     def et_workspace_size(self, Q: int, k: int, nprobe: int = 0) -> int:
         b = C.c_size_t()
         check(_lib.load().et_workspace_size(self._h, Q, k, nprobe, C.byref(b)))

@@ -144,6 +144,7 @@ struct et_index {
   et::DevBuf code[et::kMaxTrees], lcp[et::kMaxTrees];
   bool fused = false;                // forest with M <= 8: one scan over masked tuple records
   et::DevBuf fused_rec;
+  et::DevBuf narrow_rec;             // forest with 8 < M <= 16: narrow-scan tuple records (2 x uint4)
   int64_t n_leaves[et::kMaxTrees] = {};
   et::DevBuf group_off, ids, group_mult, group_minid, slot2group;
   et::DevBuf t0_tup_off, tup_leaf[et::kMaxTrees];
@@ -349,6 +350,38 @@ static int64_t build_fused(et_index* ix, const uint8_t* codes, const Groups& g, 
   return look;
 }
 
+// Narrow-scan records (narrow.cuh; forests with 8 < M <= 16): two uint4 per
+// tuple (distinct full code, lexicographic order) = 16 half-words, half-word
+// l = (code byte l) << 5 | lookup-mask bit l (the mask of build_fused: level l
+// is looked up iff l - split[u] >= LCP(tuple t-1, tuple t) over tree u's
+// bytes), half-word 0 adds floor(log2(multiplicity)) in bits 1..4; levels >= M
+// are 0.
+static void build_narrow(et_index* ix, const uint8_t* codes, const Groups& g, int M, int T, const int32_t* split) {
+  const size_t G = g.off.size() - 1;
+  std::vector<uint4> rec(2 * G);
+  for (size_t j = 0; j < G; ++j) {
+    const uint8_t* row = codes + (size_t)g.first[j] * M;
+    const uint8_t* prev = j ? codes + (size_t)g.first[j - 1] * M : nullptr;
+    uint32_t mask = 0;
+    for (int u = 0; u < T; ++u) {
+      int l = 0;
+      if (prev) while (split[u] + l < split[u + 1] && row[split[u] + l] == prev[split[u] + l]) ++l;
+      for (int b = split[u] + l; b < split[u + 1]; ++b) mask |= 1u << b;
+    }
+    const uint64_t mu = g.off[j + 1] - g.off[j];
+    uint32_t mb = 0;
+    while (mb < 15 && (2ull << mb) <= mu) ++mb;
+    uint32_t hw[16] = {};
+    for (int l = 0; l < M; ++l) hw[l] = ((uint32_t)row[l] << 5) | ((mask >> l) & 1u);
+    hw[0] |= mb << 1;
+    uint32_t w[8];
+    for (int i = 0; i < 8; ++i) w[i] = hw[2 * i] | (hw[2 * i + 1] << 16);
+    rec[2 * j] = make_uint4(w[0], w[1], w[2], w[3]);
+    rec[2 * j + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+  ix->narrow_rec.upload(rec);
+}
+
 static void finish_tree(et_index* ix, int t, HostTree& h) {
   ix->n_leaves[t] = (int64_t)h.code.size();
   ix->code[t].upload(make_records(h));
@@ -502,6 +535,7 @@ static et_index* build_forest(const uint8_t* codes_in, const int32_t* ids, int64
     scan_look = build_fused(ix.get(), codes, g, M, T, split);
     look = (double)scan_look;
   }
+  if (T > 1 && M > kMaxMT && M <= 16) build_narrow(ix.get(), codes, g, M, T, split);   // few-query scan
   for (int t = 0; t < T; ++t) { ix->stats[t].groups = (int64_t)G; ix->stats[t].scan_lookups = scan_look; }
   ix->lookups_per_query = look;
   return ix.release();
@@ -670,11 +704,17 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   pl.lut0 = (pl.MTmax == 8);
   const int64_t base = (Q + 31) / 32;
   // Cost model per unit (cycles of one SM): tables ~ nq * K * d * 2 / 128 * 1.25
-  // (fp32 lanes), scan ~ 1.5 * lookups per query / S (one warp-wide smem lookup
-  // per lookup for 32 queries).  Pick the (chunks, S) with the least makespan.
+  // (fp32 lanes), scan ~ max(1.5 * lookups, 18 * leaf steps) per query / S
+  // (one warp-wide step per leaf for 32 queries).  Pick the (chunks, S) with the
+  // least makespan.
   const double K = ix->K;
   const double d = std::max(1, ix->kind == kIvf ? ix->d : ix->M * 16);
-  const double look = std::max(1.0, ix->lookups_per_query);
+  // scan cycles of one unit: a leaf (tuple) step costs ~37 warp instructions
+  // per 32 queries on 4 schedulers at ~50% issue efficiency (~18 cycles per
+  // leaf), a lookup ~1.5 -- whichever dominates (fused forests: many tuple
+  // steps with ~1.7 lookups each)
+  const double leaves = (ix->fused || ix->T == 1) ? (double)ix->n_groups : 0.0;
+  const double look = std::max({1.0, 1.5 * ix->lookups_per_query, 18.0 * leaves});
   double best = 1e300;
   const int64_t cand_chunks[2] = {base, std::min<int64_t>(Q, ((base + nsm - 1) / nsm) * nsm)};
   const int smax = (ix->T > 1 && !ix->fused) ? 1 : 64;
@@ -684,7 +724,7 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
     for (int S = 1; S <= smax; S *= 2) {
       const int64_t units = nc * S;
       if (units > (1 << 30)) break;
-      const double per = nq * K * d * 2.0 / 128.0 * 1.25 + 1.5 * look / S + 2000.0;
+      const double per = nq * K * d * 2.0 / 128.0 * 1.25 + look / S + 2000.0;
       const double waves = std::ceil((double)units / nsm);
       const double cost = waves * per;
       if (cost < best * 0.98) { best = cost; pl.n_chunks = (int)nc; pl.S = S; }
@@ -839,6 +879,12 @@ static void table_source(ScanParams& sp, const et_index* ix, const float* codebo
     sp.s = d / ix->M;
     sp.vec4 = aligned16(queries) && aligned16(codebooks) && (d % 4 == 0) ? 1 : 0;
   }
+}
+
+// experiments: ET_NARROW=0 keeps joined forests on the per-tree scan + join
+static bool narrow_off() {
+  static const bool off = [] { const char* e = std::getenv("ET_NARROW"); return e && e[0] == '0'; }();
+  return off;
 }
 
 // Fused tables with 16 < s <= 64 (c3): the chunk-major codebook copy the wide
@@ -1010,6 +1056,19 @@ et_status et_workspace_size(const et_index* ix, int64_t Q, int32_t k, int32_t np
   ET_API_END
 }
 
+et_status et_plan_info(const et_index* ix, int64_t Q, int32_t k, int32_t* n_chunks, int32_t* S, int32_t* streams) {
+  ET_API_BEGIN
+  if (!ix || !n_chunks || !S || !streams) fail(ET_ERR_CONFIG, "null argument");
+  if (ix->kind == kIvf) fail(ET_ERR_CONFIG, "IVF plans depend on the probes (device data)");
+  if (Q < 1) fail(ET_ERR_CONFIG, "Q < 1");
+  const Plan pl = make_plan(ix, Q, k <= 0 ? 1 : k, num_sms());
+  *n_chunks = pl.n_chunks;
+  *S = k <= 0 ? 1 : pl.S;
+  const int64_t leaves = ix->fused ? ix->n_groups : ix->n_leaves[0];
+  *streams = (k > 0 && pl.MTmax == 8 && leaves / *S / kWarps >= kLongRange) ? kStreamsLong : kStreams;
+  ET_API_END
+}
+
 et_status et_etree_distances(const et_index* ix, const float* codebooks, int32_t d, const float* luts,
                              const float* queries, int64_t Q, float* out, void* workspace, size_t ws,
                              void* stream) {
@@ -1077,6 +1136,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   sp.unit_thr = w.unit_thr;
   sp.qthr = w.qthr;
   sp.qthr_shared = pl.S > 1;
+  sp.long_ranges = sp.tree[0].n_leaves / pl.S / kWarps >= kLongRange;
   cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, (cudaStream_t)stream), "qthr init");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
@@ -1097,6 +1157,22 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   // per-warp lists (the in-CTA merge costs ~5 us per CTA on c2)
   sp.compact = !fp.fast;
   fp.lpu = sp.compact ? 1 : kWarps;
+  // Narrow forest scan (narrow.cuh): forests of 8 < M <= 16 bytes when every
+  // chunk holds <= 8 queries (few queries per SM, c3) -- all 16 levels' tables
+  // in shared memory, the tuples scanned once, no per-tree partials or join;
+  // same plan, same workspace.  Lists of query slot q: lanes q + 8 g, g < 4.
+  const bool narrow = ix->narrow_rec.p && !sp.luts && sp.vec4 && narrow_supported(sp.s) && fp.fast &&
+                      pl.S == 1 && (Q + pl.n_chunks - 1) / pl.n_chunks <= 8 && !narrow_off();
+  if (narrow) {
+    sp.nrec = ix->narrow_rec.as<uint4>();
+    sp.fsplit = 0;   // the trees' first levels: per-tree partials summed in tree order (A13)
+    for (int t = 1; t < ix->T; ++t) sp.fsplit |= 1u << ix->split[t];
+    fp.lgroups = 4;
+    cuda_check(timed("scan", st, [&] { return launch_narrow(sp, st); }), "scan(narrow)");
+    cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
+    g_err.clear();
+    return ET_OK;
+  }
   // (a finalize fused into the scan kernel was measured +30 us on c2: its
   // latency-bound tail runs with the SM otherwise idle)
   cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
@@ -1152,6 +1228,7 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   sp.unit_thr = w.unit_thr;
   sp.qthr = w.qthr;
   sp.qthr_shared = 1;
+  sp.long_ranges = ix->n_groups / std::max(1, ix->nlist) / kWarps >= kLongRange;   // mean list per warp
   cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, st), "qthr init");
   const bool ivf_fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
   sp.compact = !ivf_fast;

@@ -17,7 +17,9 @@ constexpr int kKMax = 256;                 // codewords per subspace (one byte, 
 constexpr int kTopkMax = 256;              // largest k of the fused top-k
 constexpr int kFinWarps = 8;               // warps per finalize CTA
 constexpr int kStreams = 4;                // lockstep leaf streams per scan warp (8 warps: 32 chains per SM)
-constexpr int kBatchEmit = 32 * kStreams;  // candidates a lane can append between two buffer checks
+constexpr int kStreamsLong = 6;            // ... for long leaf ranges (>= kLongRange leaves per warp, host plan)
+constexpr int kLongRange = 384;
+constexpr int kBatchEmit = 32 * kStreamsLong;  // candidates a lane can append between two buffer checks
 
 // One tree of the device layout ("leaf-major HMS"): the leaves in
 // depth-first (= lexicographic) order, each with its full projected code and
@@ -40,6 +42,7 @@ struct FinParams {
   int64_t Q = 0;
   int k = 0, B = 0, S = 1;
   int lpu = kWarps;                   // candidate lists per unit (1: compacted by the scan kernel)
+  int lgroups = 1;                    // lane groups per query slot (narrow scan: 4, lanes q + 8 g)
   const int* qslot_off = nullptr;     // [Q+1]
   const int* qslot = nullptr;         // chunk*32 + lane for each (query, probe)
   int flat_nchunks = 0;               // > 0: one slot per query, computed from the flat chunking
@@ -67,6 +70,7 @@ struct ScanParams {
   const float* queries = nullptr;     // [Q][d]           (fused tables)
   const float* luts = nullptr;        // [Q][M][K]        (materialised tables) or null
   const float4* cbt = nullptr;        // [M][s/4][K] chunk-major codebook copy (16 < s <= 64) or null
+  const uint4* nrec = nullptr;        // narrow forest records, 2 per tuple (narrow.cuh) or null
   const float* coarse = nullptr;      // [nlist][d]       (IVF residual tables) or null
   const int* layer_sub = nullptr;     // [M] subspace of each code byte (chunk order), device copy
   int lsub[kMaxTrees * kMaxMT] = {};  // the same, by value (kernel parameters: no dependent load)
@@ -106,6 +110,7 @@ struct ScanParams {
   int vec4 = 1;                       // query/codebook rows 16-byte aligned
   int compact = 0;                    // merge each lane's 16 per-warp lists at the end (long lists)
   int wide_old = 0;                   // experiments (ET_WIDE_OLD=1): s > 16 8-level trees use build_tables_wide
+  int long_ranges = 0;                // >= kLongRange leaves per scan warp: kStreamsLong streams (top-k)
   // ---- fused E-Forest (M <= 8) ----
   int masked = 0;                     // records carry a per-level lookup mask (fused forest tuple records)
   uint32_t fsplit = 0;                // bit l set: level l starts a forest tree (partials summed in tree order)
@@ -133,6 +138,9 @@ __host__ __device__ inline ScanSmem scan_smem(int MTmax) {
 
 // ---- launchers (kernels.cu); each returns cudaGetLastError() ----
 cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st);
+// narrow forest scan (<= 8 queries per CTA, 8 < M <= 16, s in {16, 60}); false if no instantiation
+bool narrow_supported(int s);
+cudaError_t launch_narrow(const ScanParams& p, cudaStream_t st);
 cudaError_t launch_finalize(const FinParams& p, cudaStream_t st);
 cudaError_t launch_fill_flat(int64_t Q, int n_chunks, int* chunk_q, int* qslot_off, int* qslot,
                              cudaStream_t st);

@@ -22,6 +22,14 @@ cudaError_t launch_scan_60(const ScanParams& p, size_t smem, cudaStream_t st);
 cudaError_t launch_scan_0(const ScanParams& p, size_t smem, cudaStream_t st);
 
 // K2 dispatch by sub-vector length (template instantiations live in scan_s*.cu)
+cudaError_t launch_narrow_16(const ScanParams& p, cudaStream_t st);
+cudaError_t launch_narrow_60(const ScanParams& p, cudaStream_t st);
+bool narrow_supported(int s) { return s == 16 || s == 60; }
+cudaError_t launch_narrow(const ScanParams& p, cudaStream_t st) {
+  if (p.n_units <= 0) return cudaSuccess;
+  return p.s == 60 ? launch_narrow_60(p, st) : launch_narrow_16(p, st);
+}
+
 cudaError_t launch_scan(const ScanParams& p, int MTmax, cudaStream_t st) {
   if (p.n_units <= 0) return cudaSuccess;
   const size_t smem = scan_smem(MTmax).total;
@@ -90,11 +98,13 @@ __device__ __forceinline__ int fin_slot(const FinParams& p, int64_t q, int j) {
 // (slot, leaf segment, scan warp).  Its count is cand_cnt[list], its entries
 // cand[list * B ...] (the scan kernel's per-warp, per-lane buffers).
 __device__ __forceinline__ size_t fin_list(const FinParams& p, int64_t q, int s0, int li) {
-  const int per = p.S * p.lpu;
+  const int lpg = p.lpu * p.lgroups;          // lists per (unit, slot)
+  const int per = p.S * lpg;
   const int j = li / per, r = li - j * per;
-  const int sg = r / p.lpu, w = r - sg * p.lpu;
+  const int sg = r / lpg, r2 = r - sg * lpg;
+  const int g = r2 / p.lpu, w = r2 - g * p.lpu;
   const int slot = fin_slot(p, q, s0 + j);
-  return ((size_t)((slot >> 5) * p.S + sg) * 32 + (slot & 31)) * kWarps + w;
+  return ((size_t)((slot >> 5) * p.S + sg) * 32 + (slot & 31) + 8 * g) * kWarps + w;
 }
 
 // Enumerates the candidates of query q: smem copy when they fit, else global.
@@ -121,7 +131,7 @@ struct CandSrc {
     // 32 lists per round: counts loaded in parallel (lane = list), then the
     // round's entries spread over the lanes (binary search on the prefix)
     const uint32_t tb = __float_as_uint(thr);
-    const int nl = (s1 - s0) * p->S * p->lpu;
+    const int nl = (s1 - s0) * p->S * p->lpu * p->lgroups;
     for (int l0 = 0; l0 < nl; l0 += 32) {
       const int li = l0 + lane;
       size_t ul = 0;
@@ -187,7 +197,7 @@ __device__ void finalize_query(const FinParams& p, FinWarp& fw, int64_t q) {
     uint32_t* K_ = fw.key;
     uint32_t* G_ = fw.grp;
     uint32_t* U_ = fw.mul;
-    const int nl = (s1 - s0) * p.S * p.lpu;
+    const int nl = (s1 - s0) * p.S * p.lpu * p.lgroups;
     for (int l0 = 0; l0 < nl && !overflow; l0 += 32) {
       const int li = l0 + lane;
       size_t ul = 0;
@@ -554,7 +564,7 @@ __device__ __forceinline__ void finalize_fast_query(const FinParams& p, int64_t 
   uint2 r0 = make_uint2(0xffffffffu, 0), r1 = make_uint2(0xffffffffu, 0);
   int n = 0;
   bool overflow = false;
-  const int nl = (s1 - s0) * p.S * p.lpu;
+  const int nl = (s1 - s0) * p.S * p.lpu * p.lgroups;
   for (int l0 = 0; l0 < nl && !overflow; l0 += 32) {
     const int li = l0 + lane;
     size_t ul = 0;

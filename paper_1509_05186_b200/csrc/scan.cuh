@@ -259,11 +259,17 @@ __device__ __forceinline__ void stage_async(const ScanParams& p, int t, int chun
                                             uint32_t stage_s) {
   const TreeDev& tr = p.tree[t];
   const int j = threadIdx.x & (SS - 1);
+  // arithmetic chunking: the chunk's queries are rows [s0, s1) (bounds once,
+  // not per slot: two 64-bit divisions)
+  int64_t s0 = 0, s1 = 0;
+  if (p.flatQ > 0) {
+    s0 = (int64_t)chunk * p.flatQ / nch;
+    s1 = (int64_t)(chunk + 1) * p.flatQ / nch;
+  }
 #pragma unroll
   for (int i = threadIdx.x >> 4; i < 32; i += kThreads / SS) {   // query slot i, dimension j
     int q = -1;
     if (p.flatQ > 0) {
-      const int64_t s0 = (int64_t)chunk * p.flatQ / nch, s1 = (int64_t)(chunk + 1) * p.flatQ / nch;
       q = (s0 + i < s1) ? (int)(s0 + i) : -1;
     } else {
       q = __ldg(p.chunk_q + (size_t)chunk * 32 + i);
@@ -1151,15 +1157,24 @@ __device__ __forceinline__ void tmem_rec_ld(uint32_t tq, const uint4& r, uint32_
 }
 template <int NS>
 __device__ __forceinline__ void tmem_wait_all(uint32_t (&t0)[NS], uint32_t (&t1)[NS]) {
-  static_assert(NS == 1 || NS == 2 || NS == 4, "streams");
+  static_assert(NS == 1 || NS == 2 || NS == 4 || NS == 6 || NS == 8, "streams");
   if constexpr (NS == 1) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0[0]), "+r"(t1[0]));
   } else if constexpr (NS == 2) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(t0[0]), "+r"(t1[0]), "+r"(t0[1]), "+r"(t1[1]));
-  } else {
+  } else if constexpr (NS == 4) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+r"(t0[0]), "+r"(t1[0]), "+r"(t0[1]), "+r"(t1[1]), "+r"(t0[2]), "+r"(t1[2]), "+r"(t0[3]),
                    "+r"(t1[3]));
+  } else if constexpr (NS == 6) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(t0[0]), "+r"(t1[0]), "+r"(t0[1]), "+r"(t1[1]), "+r"(t0[2]), "+r"(t1[2]), "+r"(t0[3]),
+                   "+r"(t1[3]), "+r"(t0[4]), "+r"(t1[4]), "+r"(t0[5]), "+r"(t1[5]));
+  } else {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(t0[0]), "+r"(t1[0]), "+r"(t0[1]), "+r"(t1[1]), "+r"(t0[2]), "+r"(t1[2]), "+r"(t0[3]),
+                   "+r"(t1[3]), "+r"(t0[4]), "+r"(t1[4]), "+r"(t0[5]), "+r"(t1[5]), "+r"(t0[6]), "+r"(t1[6]),
+                   "+r"(t0[7]), "+r"(t1[7]));
   }
 }
 
@@ -1495,17 +1510,17 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
 }
 
 
-template <int MT, bool MASKED>
+template <int MT, bool MASKED, int NS = kStreams>
 __device__ __forceinline__ void scan_tree3_mode(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a,
                                                 uint32_t b) {
   // fused forests of two 4-level trees (the c5 split 0-3 | 4-7): the tree
   // boundary at compile time
   if (MASKED && MT == 8 && e.p->fsplit == (1u << 4)) {
-    if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, kStreams, 4>(e, sm, tr, a, b);
+    if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, NS, 4>(e, sm, tr, a, b);
     else scan_tree3<MT, MASKED, false, kStreams, 4>(e, sm, tr, a, b);
     return;
   }
-  if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, kStreams, 0>(e, sm, tr, a, b);
+  if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, NS, 0>(e, sm, tr, a, b);
   else scan_tree3<MT, MASKED, false, kStreams, 0>(e, sm, tr, a, b);
 }
 
@@ -1616,7 +1631,11 @@ __device__ __forceinline__ void scan_any(EmitCtx& e, const SmemScan& sm, const T
 // MODE 0: one E-Tree (or IVF lists); 1: E-Forest with per-tree partials and
 // the tuple join (M > 8, e.g. c3); 2: fused E-Forest over masked tuple
 // records (M <= 8, e.g. c5).
-template <int SS, int MTC, int MODE>
+// NS: lockstep streams per warp of the 8-level top-k scans (kStreamsLong for
+// long leaf ranges, p.long_ranges: more independent chains per warp; short
+// ranges keep kStreams -- a separate instantiation, so neither pays the other's
+// registers or code).
+template <int SS, int MTC, int MODE, int NS = kStreams>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant__ ScanParams p) {
   constexpr bool FOREST = (MODE == 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1765,7 +1784,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       if constexpr (FOREST) {
         scan_any<MTC, 0>(e, sm, tr, wa, wb, lut0g);   // per-leaf partials of every tree
       } else if constexpr (MTC > 0) {
-        scan_tree3_mode<MTC, MODE == 2>(e, sm, tr, wa, wb);
+        scan_tree3_mode<MTC, MODE == 2, NS>(e, sm, tr, wa, wb);
       } else {
         scan2_dispatch<MODE == 2>(e, sm, tr, wa, wb);
       }
@@ -1875,12 +1894,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
 }
 
 
-template <int SS, int MTC, int MODE>
+template <int SS, int MTC, int MODE, int NS = kStreams>
 static cudaError_t launch_scan_t(const ScanParams& p, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS, MTC, MODE>,
+  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS, MTC, MODE, NS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  scan_kernel<SS, MTC, MODE><<<p.n_units, kThreads, smem, st>>>(p);
+  scan_kernel<SS, MTC, MODE, NS><<<p.n_units, kThreads, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -1898,11 +1917,13 @@ cudaError_t launch_scan_s(const ScanParams& p, size_t smem, cudaStream_t st) {
   }
   if (p.masked) {  // fused forest
     if constexpr (SS != 60) {
-      if (mt == 8) return launch_scan_t<SS, 8, 2>(p, smem, st);
+      if (mt == 8) return p.long_ranges ? launch_scan_t<SS, 8, 2, kStreamsLong>(p, smem, st)
+                                        : launch_scan_t<SS, 8, 2>(p, smem, st);
     }
     return launch_scan_t<SS, 0, 2>(p, smem, st);
   }
-  if (mt == 8) return launch_scan_t<SS, 8, 0>(p, smem, st);
+  if (mt == 8) return p.long_ranges ? launch_scan_t<SS, 8, 0, kStreamsLong>(p, smem, st)
+                                    : launch_scan_t<SS, 8, 0>(p, smem, st);
   if (mt == 4) return launch_scan_t<SS, 4, 0>(p, smem, st);
   return launch_scan_t<SS, 0, 0>(p, smem, st);
 }

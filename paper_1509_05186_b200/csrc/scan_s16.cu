@@ -1,9 +1,11 @@
 // scan_s16.cu -- scan kernel instantiations for sub-vector length s = 16
 // (one translation unit per s so the kernel variants compile in parallel).
 #include "scan.cuh"
+#include "narrow.cuh"
 
 namespace et {
 cudaError_t launch_scan_16(const ScanParams& p, size_t smem, cudaStream_t st) { return launch_scan_s<16>(p, smem, st); }
+cudaError_t launch_narrow_16(const ScanParams& p, cudaStream_t st) { return launch_narrow_s<16>(p, st); }
 }  // namespace et
 
 #ifdef ET_PHASE_TIMING
