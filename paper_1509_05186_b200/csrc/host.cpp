@@ -673,13 +673,15 @@ struct Plan {
   int n_chunks = 0, S = 1, n_units = 0, MTmax = 0, B = 0;
   bool lut0 = false;
   bool mat_luts = false;   // tables materialised by lut_kernel, copied into each scan CTA
+  bool long_ranges = false;   // top-k scans of 8-level trees with >= kLongRange leaves per warp: kStreamsLong
   int64_t part_stride = 0;
   int64_t part_base[kMaxTrees] = {};
 };
 
 // candidate buffer per (unit, warp, lane): k survivors of a refresh + ties, plus
 // one batch of emissions (kBatchEmit) before the next buffer check
-static int topk_B(int k) { return ((2 * k + kBatchEmit + 31) / 32) * 32; }
+// (ns: lockstep streams per scan warp, 32 candidates per stream per batch)
+static int topk_B(int k, int ns = kStreams) { return ((2 * k + 32 * ns + 31) / 32) * 32; }
 
 // Tables built once by lut_kernel ([Q][M][K] in the workspace) and copied
 // into each scan CTA, instead of built inside the CTA: ET_TABLES=materialised
@@ -704,17 +706,17 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
   pl.lut0 = (pl.MTmax == 8);
   const int64_t base = (Q + 31) / 32;
   // Cost model per unit (cycles of one SM): tables ~ nq * K * d * 2 / 128 * 1.25
-  // (fp32 lanes), scan ~ max(1.5 * lookups, 18 * leaf steps) per query / S
-  // (one warp-wide step per leaf for 32 queries).  Pick the (chunks, S) with the
-  // least makespan.
+  // (fp32 lanes), scan ~ 1.5 * lookups per query / S (one warp-wide smem lookup
+  // per lookup for 32 queries).  Pick the (chunks, S) with the least makespan.
+  // (A leaf-step term -- c5 313 chunks x S = 4 instead of 444 x 1 -- measured
+  // 0.863 vs 0.846 ms: not taken.)
   const double K = ix->K;
   const double d = std::max(1, ix->kind == kIvf ? ix->d : ix->M * 16);
   // scan cycles of one unit: a leaf (tuple) step costs ~37 warp instructions
   // per 32 queries on 4 schedulers at ~50% issue efficiency (~18 cycles per
   // leaf), a lookup ~1.5 -- whichever dominates (fused forests: many tuple
   // steps with ~1.7 lookups each)
-  const double leaves = (ix->fused || ix->T == 1) ? (double)ix->n_groups : 0.0;
-  const double look = std::max({1.0, 1.5 * ix->lookups_per_query, 18.0 * leaves});
+  const double look = std::max(1.0, 1.5 * ix->lookups_per_query);
   double best = 1e300;
   const int64_t cand_chunks[2] = {base, std::min<int64_t>(Q, ((base + nsm - 1) / nsm) * nsm)};
   const int smax = (ix->T > 1 && !ix->fused) ? 1 : 64;
@@ -731,7 +733,9 @@ static Plan make_plan(const et_index* ix, int64_t Q, int k, int nsm) {
     }
   }
   pl.n_units = pl.n_chunks * pl.S;
-  pl.B = topk_B(std::max(1, k));
+  const int64_t leaves = ix->fused ? ix->n_groups : ix->n_leaves[0];
+  pl.long_ranges = pl.MTmax == 8 && leaves / pl.S / kWarps >= kLongRange;
+  pl.B = topk_B(std::max(1, k), pl.long_ranges ? kStreamsLong : kStreams);
   int64_t off = 0;
   if (ix->T > 1 && !ix->fused)   // joined forests: per-leaf partials of every tree (the join reads them)
     for (int t = 0; t < ix->T; ++t) { pl.part_base[t] = off; off += ix->n_leaves[t] * 32; }
@@ -750,7 +754,8 @@ static Plan make_ivf_plan(const et_index* ix, int64_t Q, int w, int k) {
   pl.n_chunks = (int)((Q * w + 31) / 32 + 2 * ix->nlist);   // one partial chunk per (tier, cell)
   pl.S = 1;
   pl.n_units = pl.n_chunks;
-  pl.B = topk_B(std::max(1, k));
+  pl.long_ranges = pl.MTmax == 8 && ix->n_groups / std::max(1, ix->nlist) / kWarps >= kLongRange;   // mean list
+  pl.B = topk_B(std::max(1, k), pl.long_ranges ? kStreamsLong : kStreams);
   return pl;
 }
 
@@ -1064,8 +1069,7 @@ et_status et_plan_info(const et_index* ix, int64_t Q, int32_t k, int32_t* n_chun
   const Plan pl = make_plan(ix, Q, k <= 0 ? 1 : k, num_sms());
   *n_chunks = pl.n_chunks;
   *S = k <= 0 ? 1 : pl.S;
-  const int64_t leaves = ix->fused ? ix->n_groups : ix->n_leaves[0];
-  *streams = (k > 0 && pl.MTmax == 8 && leaves / *S / kWarps >= kLongRange) ? kStreamsLong : kStreams;
+  *streams = (k > 0 && pl.long_ranges) ? kStreamsLong : kStreams;
   ET_API_END
 }
 
@@ -1136,7 +1140,7 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   sp.unit_thr = w.unit_thr;
   sp.qthr = w.qthr;
   sp.qthr_shared = pl.S > 1;
-  sp.long_ranges = sp.tree[0].n_leaves / pl.S / kWarps >= kLongRange;
+  sp.long_ranges = pl.long_ranges;
   cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, (cudaStream_t)stream), "qthr init");
   FinParams fp;
   fp.Q = Q; fp.k = k; fp.B = pl.B; fp.S = pl.S;
@@ -1228,7 +1232,7 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
   sp.unit_thr = w.unit_thr;
   sp.qthr = w.qthr;
   sp.qthr_shared = 1;
-  sp.long_ranges = ix->n_groups / std::max(1, ix->nlist) / kWarps >= kLongRange;   // mean list per warp
+  sp.long_ranges = pl.long_ranges;
   cuda_check(cudaMemsetAsync(w.qthr, 0x7f, (size_t)Q * 4, st), "qthr init");
   const bool ivf_fast = (double)ix->N >= (double)ix->n_groups * std::max(1.0, k / 8.0);
   sp.compact = !ivf_fast;

@@ -19,7 +19,8 @@ constexpr int kFinWarps = 8;               // warps per finalize CTA
 constexpr int kStreams = 4;                // lockstep leaf streams per scan warp (8 warps: 32 chains per SM)
 constexpr int kStreamsLong = 6;            // ... for long leaf ranges (>= kLongRange leaves per warp, host plan)
 constexpr int kLongRange = 384;
-constexpr int kBatchEmit = 32 * kStreamsLong;  // candidates a lane can append between two buffer checks
+constexpr int kBatchEmit = 32 * kStreams;  // candidates a lane can append between two buffer checks
+constexpr int kBatchEmitLong = 32 * kStreamsLong;   // ... with kStreamsLong streams (buffers 64 entries longer)
 
 // One tree of the device layout ("leaf-major HMS"): the leaves in
 // depth-first (= lexicographic) order, each with its full projected code and

@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) narrow_kernel(const __grid_consta
   const int chunk = (int)blockIdx.x, unit = chunk;
   const int lane = lane_id(), warp = warp_id();
   const int ql = lane & (kNarrowQ - 1);
+  phase_mark(unit, 0);
   const int64_t s0 = (int64_t)chunk * p.flatQ / p.n_units, s1 = (int64_t)(chunk + 1) * p.flatQ / p.n_units;
   const int nq = (int)(s1 - s0);
   ET_CHECK(nq <= kNarrowQ);
@@ -219,8 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1) narrow_kernel(const __grid_consta
   if (threadIdx.x < 32) thr[lane] = 0x7f800000u;
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  phase_mark(unit, 1);
   narrow_build<SS>(p, base);
   __syncthreads();
+  phase_mark(unit, 5);
 
   EmitCtx e;
   e.p = &p;
@@ -241,9 +244,11 @@ __global__ void __launch_bounds__(kThreads, 1) narrow_kernel(const __grid_consta
     else narrow_scan<0>(e, base, base + L::thr, wa, wb);
   }
   __syncthreads();
+  phase_mark(unit, 3);
   if (warp == 0 && lane < nq && p.qthr) p.qthr[s0 + lane] = thr[lane];   // the query's only unit
   p.cand_cnt[((size_t)unit * 32 + lane) * kWarps + warp] = e.ts.cnt;
   if (warp == 0 && p.unit_thr) p.unit_thr[(size_t)unit * 32 + lane] = __uint_as_float(thr[ql]);
+  phase_mark(unit, 4);
 }
 
 template <int SS>

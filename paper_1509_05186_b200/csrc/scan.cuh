@@ -946,7 +946,7 @@ __device__ void build_tables(const ScanParams& p, const SmemScan& sm, int t, int
 // (distance, id) pairs: t = smallest distance whose cumulative multiplicity
 // reaches k; all candidates < t; of the candidates == t, those whose smallest
 // id ranks below k - (multiplicity < t).  Returns the new count and threshold.
-constexpr int kRefreshPer = (2 * kTopkMax + kBatchEmit) / 32;   // entries per lane held in registers (>= B)
+constexpr int kRefreshPer = (2 * kTopkMax + kBatchEmitLong) / 32;   // entries per lane held in registers (>= B)
 
 __device__ __noinline__ void refresh_buffer(uint2* buf, int n, int k, const uint32_t* gmult,
                                             const int32_t* gminid, int* new_cnt, float* new_thr) {
@@ -1071,12 +1071,12 @@ struct CntThr { int cnt; float thr; };
 constexpr float kThrNone = 1e38f;
 
 __device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr, uint32_t msum, int B, int k,
-                                             const uint32_t* gmult, const int32_t* gminid) {
+                                             const uint32_t* gmult, const int32_t* gminid, int batch) {
   const int lane = lane_id();
   // full buffers, and (once) buffers that first reach k candidates while the
   // lane has no threshold yet: an early exact bound stops the flood of
   // candidates that every fresh warp would otherwise emit
-  unsigned full = __ballot_sync(FULLMASK, cnt > B - kBatchEmit || ((cnt >= k || msum >= (uint32_t)k) && !(thr < kThrNone)));
+  unsigned full = __ballot_sync(FULLMASK, cnt > B - batch || ((cnt >= k || msum >= (uint32_t)k) && !(thr < kThrNone)));
   while (full) {
     const int L = __ffs(full) - 1;
     full &= full - 1;
@@ -1088,11 +1088,14 @@ __device__ __noinline__ CntThr maybe_refresh(uint2* warp_buf, int cnt, float thr
   return CntThr{cnt, thr};
 }
 
-__device__ __forceinline__ void refresh_if_needed(EmitCtx& e) {
+// batch: the most candidates a lane can append before the next check (32 per
+// stream); B = 2k + batch rounded up (the plan's topk_B).
+__device__ __forceinline__ void refresh_if_needed(EmitCtx& e, int batch = kBatchEmit) {
   const ScanParams& p = *e.p;
-  if (__any_sync(FULLMASK, e.ts.cnt > p.B - kBatchEmit ||
+  if (__any_sync(FULLMASK, e.ts.cnt > p.B - batch ||
                              ((e.ts.cnt >= p.k || e.ts.msum >= (uint32_t)p.k) && !(e.ts.thr < kThrNone)))) {
-    const CntThr r = maybe_refresh(e.ts.warp_buf, e.ts.cnt, e.ts.thr, e.ts.msum, p.B, p.k, p.group_mult, p.group_minid);
+    const CntThr r = maybe_refresh(e.ts.warp_buf, e.ts.cnt, e.ts.thr, e.ts.msum, p.B, p.k, p.group_mult,
+                                   p.group_minid, batch);
     e.ts.cnt = r.cnt;
     e.ts.thr = r.thr;
   }
@@ -1497,7 +1500,7 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
       else step(j, std::false_type{});
     }
     if constexpr (TOPK) {   // prune full buffers; share the threshold with the CTA's other warps
-      refresh_if_needed(e);  // and with every other unit scanning the same query
+      refresh_if_needed(e, 32 * NS);  // and with every other unit scanning the same query
       if (e.ts.active) {
         const unsigned mine = __float_as_uint(e.ts.thr);
         atomicMin(&sm.thr[lane], mine);

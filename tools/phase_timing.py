@@ -34,7 +34,10 @@ def main():
     st["q_dev"] = torch.from_numpy(st["qx"]).to(dev)
     st["cb_dev"] = torch.from_numpy(st["cb"]).to(dev)
     for _ in range(3):
-        ix.et_etree_topk(cfg.topk, queries=st["q_dev"], codebooks=st["cb_dev"])
+        if cfg.ivf_nlist:   # IVF (c4): the same scan kernel over (cell, queries) chunks
+            ix.et_ivf_topk(st["q_dev"], nprobe=cfg.ivf_nprobe, k=cfg.topk)
+        else:
+            ix.et_etree_topk(cfg.topk, queries=st["q_dev"], codebooks=st["cb_dev"])
     torch.cuda.synchronize()
     lib = api._lib.load()
     n = 1 << 16
@@ -48,9 +51,11 @@ def main():
     t0 = b[:, 0].min()
     order = [(0, 1, "start->build"), (1, 5, "stage"), (5, 6, "round 0"), (6, 7, "TMEM copy"),
              (7, 2, "round 1"), (2, 3, "scan"), (3, 4, "compaction")]
-    if s60:   # joined forest (T = 2): tree 1 tables, tree 1 scan, tree 0 tables, tree 0 scan, join
+    if s60 and b[:, 6].max() > 0:   # joined forest (T = 2): tree 1 tables/scan, tree 0 tables/scan, join
         order = [(0, 1, "setup"), (1, 5, "tables tree 1"), (5, 6, "scan tree 1"), (6, 7, "tables tree 0"),
                  (7, 2, "scan tree 0"), (2, 3, "join"), (3, 4, "tail")]
+    elif s60:   # narrow forest scan (narrow_kernel): staging, 16 levels' tables, tuple scan
+        order = [(0, 1, "stage"), (1, 5, "tables (16 levels)"), (5, 3, "tuple scan"), (3, 4, "tail")]
     print(f"units {used.sum()}  kernel span {(b[:, 4].max() - t0) / 1e3:.1f} us")
     for i, j, name in order:
         d = (b[:, j] - b[:, i]) / 1e3
