@@ -1115,11 +1115,14 @@ cudaError_t launch_probe(const float* cT, int nlist, int d, const float* queries
 // IVF pair bucketing: (query, probe) pairs grouped by cell into chunks of 32
 // lanes so a warp scans one list's tree for 32 residual tables at once.
 // ---------------------------------------------------------------------------
-// Pairs are bucketed by (tier, cell): tier 0 holds every query's nearest
-// probe (rank 0), tier 1 the other probes.  Tier-0 chunks come first in the
-// chunk order, so the scan of a query's nearest list -- where its nearest
-// codes most likely are -- runs in the first waves and leaves a tight k-th
-// distance bound in qthr for the query's other probes.
+// Pairs are counted by (tier, cell): tier 0 holds every query's nearest
+// probe (rank 0), tier 1 the other probes.  A cell's pairs then form one list
+// -- its tier-0 pairs first -- cut into chunks of 32; every cell's FIRST chunk
+// comes first in the chunk order (region A), the cells' remaining chunks after
+// (region B).  So the scan of a query's nearest list -- where its nearest codes
+// most likely are -- runs in the first waves and leaves a tight k-th distance
+// bound in qthr for the query's other probes, and a cell costs ceil(n / 32)
+// chunk scans rather than one per tier (c4: ~4 -> ~3 per cell).
 __device__ __forceinline__ int ivf_entry(const int32_t* probes, int64_t i, int w, int nlist) {
   return ((i % w) == 0 ? 0 : nlist) + probes[i];
 }
@@ -1130,48 +1133,59 @@ __global__ void ivf_count_kernel(const int32_t* __restrict__ probes, int64_t P, 
   if (i < P) pair_pos[i] = atomicAdd(&cell_cnt[ivf_entry(probes, i, w, nlist)], 1);
 }
 
+// chunk_off[c] = the cell's first chunk (region A), chunk_off[nlist + c] = the
+// first of its remaining chunks (region B); chunk_off[2 nlist] = total.
 __global__ void __launch_bounds__(1024) ivf_chunks_kernel(const int* __restrict__ cell_cnt, int nlist,
                                                           const uint32_t* __restrict__ list_leaf_off,
                                                           int* chunk_off, int* n_chunks, int* chunk_cell,
                                                           uint32_t* chunk_lo, uint32_t* chunk_hi) {
-  __shared__ int part[1024];
+  __shared__ int pa[1024], pb[1024];
   const int t = threadIdx.x;
-  const int ne = 2 * nlist;                           // (tier, cell) entries, tier-major
-  const int per = (ne + blockDim.x - 1) / blockDim.x;
-  const int c0 = min(ne, t * per), c1 = min(ne, c0 + per);
-  int loc = 0;
-  for (int c = c0; c < c1; ++c) loc += (cell_cnt[c] + 31) >> 5;
-  part[t] = loc;
-  __syncthreads();
-  for (int o = 1; o < (int)blockDim.x; o <<= 1) {   // Hillis-Steele inclusive scan
-    const int v = (t >= o) ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += v;
-    __syncthreads();
-  }
-  int run = part[t] - loc;
+  const int per = (nlist + blockDim.x - 1) / blockDim.x;
+  const int c0 = min(nlist, t * per), c1 = min(nlist, c0 + per);
+  int la = 0, lb = 0;
   for (int c = c0; c < c1; ++c) {
-    chunk_off[c] = run;
-    const int nc = (cell_cnt[c] + 31) >> 5;
-    const int cell = c < nlist ? c : c - nlist;
-    for (int j = 0; j < nc; ++j) {
-      chunk_cell[run + j] = cell;
-      chunk_lo[run + j] = list_leaf_off[cell];
-      chunk_hi[run + j] = list_leaf_off[cell + 1];
-    }
-    run += nc;
+    const int n = cell_cnt[c] + cell_cnt[nlist + c];
+    la += n > 0 ? 1 : 0;
+    lb += n > 0 ? ((n + 31) >> 5) - 1 : 0;
   }
-  if (t == blockDim.x - 1) { chunk_off[ne] = part[t]; *n_chunks = part[t]; }
+  pa[t] = la;
+  pb[t] = lb;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {   // Hillis-Steele inclusive scans
+    const int va = (t >= o) ? pa[t - o] : 0, vb = (t >= o) ? pb[t - o] : 0;
+    __syncthreads();
+    pa[t] += va;
+    pb[t] += vb;
+    __syncthreads();
+  }
+  const int total_a = pa[blockDim.x - 1];
+  int ra = pa[t] - la, rb = total_a + pb[t] - lb;
+  for (int c = c0; c < c1; ++c) {
+    const int n = cell_cnt[c] + cell_cnt[nlist + c];
+    const int nb = n > 0 ? ((n + 31) >> 5) - 1 : 0;
+    chunk_off[c] = n > 0 ? ra : -1;
+    chunk_off[nlist + c] = rb;
+    if (n > 0) {
+      chunk_cell[ra] = c; chunk_lo[ra] = list_leaf_off[c]; chunk_hi[ra] = list_leaf_off[c + 1];
+      ++ra;
+    }
+    for (int j = 0; j < nb; ++j) {
+      chunk_cell[rb + j] = c; chunk_lo[rb + j] = list_leaf_off[c]; chunk_hi[rb + j] = list_leaf_off[c + 1];
+    }
+    rb += nb;
+  }
+  if (t == blockDim.x - 1) { chunk_off[2 * nlist] = total_a + pb[t]; *n_chunks = total_a + pb[t]; }
 }
 
 __global__ void ivf_scatter_kernel(const int32_t* __restrict__ probes, int64_t Q, int w, int nlist,
-                                   const int* __restrict__ pair_pos,
+                                   const int* __restrict__ cell_cnt, const int* __restrict__ pair_pos,
                                    const int* __restrict__ chunk_off, int* chunk_q, int* qslot_off, int* qslot) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < Q * w) {
-    const int c = ivf_entry(probes, i, w, nlist);
-    const int p = pair_pos[i];
-    const int ch = chunk_off[c] + (p >> 5);
+    const int cell = probes[i];
+    const int p = ((i % w) == 0) ? pair_pos[i] : cell_cnt[cell] + pair_pos[i];   // tier-0 pairs first
+    const int ch = (p < 32) ? chunk_off[cell] : chunk_off[nlist + cell] + (p >> 5) - 1;
     const int ln = p & 31;
     chunk_q[(size_t)ch * 32 + ln] = (int)(i / w);
     qslot[i] = ch * 32 + ln;
@@ -1191,8 +1205,8 @@ cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist
   ivf_chunks_kernel<<<1, 1024, 0, st>>>(cell_cnt, nlist, list_leaf_off, chunk_off, n_chunks, chunk_cell,
                                         chunk_lo, chunk_hi);
   const int64_t n = (P > Q + 1) ? P : Q + 1;
-  ivf_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(probes, Q, w, nlist, pair_pos, chunk_off, chunk_q,
-                                                                   qslot_off, qslot);
+  ivf_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(probes, Q, w, nlist, cell_cnt, pair_pos, chunk_off,
+                                                                   chunk_q, qslot_off, qslot);
   count_launch(3);
   return cudaGetLastError();
 }
