@@ -202,6 +202,24 @@ et_status et_etree_topk(const et_index* index, const float* codebooks, int32_t d
                         int32_t k, float* dist, int32_t* ids, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* Leaf extra byte ("we quantized on the extra information to 1
+ * Byte ... and store the extra information on the leaf node"; for Additive
+ * Quantization it is Eq. 1's non-zero third term).
+ * et_index_set_extra attaches one byte per database vector to a single E-Tree
+ * index: extra = HOST uint8 [n], slot order of the codes given to the build,
+ * n == N.  The byte lives on the leaf, so it must be a function of the code.
+ * Errors: ET_ERR_CONFIG (not a single tree), ET_ERR_DIMENSION (n != N),
+ * ET_ERR_INVALID_CODE (two vectors with the same code and different bytes).
+ * et_etree_topk_extra is et_etree_topk with dist = (sum_m T[m][code[m]]) +
+ * extra_table[e] (extra_table: DEVICE fp32 [256], entries >= 0 -- a
+ * quantizer's decode table shifted to start at 0; 8-level trees).  Errors as
+ * et_etree_topk, plus ET_ERR_CONFIG without extra bytes. */
+et_status et_index_set_extra(et_index* index, const uint8_t* extra, int64_t n);
+et_status et_etree_topk_extra(const et_index* index, const float* codebooks, int32_t d,
+                              const float* luts, const float* queries, int64_t Q, int32_t k,
+                              const float* extra_table, float* dist, int32_t* ids,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
 /* IVF search: probe the nprobe nearest coarse cells (fp32 direct difference,
  * ties -> lower cell), residual tables per (query, cell), per-list E-Tree
  * scan, fused top-k.  probes: optional DEVICE int32 [Q][nprobe] output.

@@ -184,8 +184,15 @@ class Index:
         return ws
 
     # ---------------------------------------------------------------- queries
-    def et_etree_topk(self, k: int, queries=None, codebooks=None, luts=None, out=None, stream=None):
-        """(dist [Q,k] fp32, ids [Q,k] int32) on the queries' device."""
+    def et_index_set_extra(self, extra) -> None:
+        """Leaf extra byte per database vector: uint8 [N] (host)."""
+        e = np.ascontiguousarray(extra, dtype=np.uint8)
+        check(_lib.load().et_index_set_extra(self._h, e.ctypes.data, int(e.shape[0])))
+
+    def et_etree_topk(self, k: int, queries=None, codebooks=None, luts=None, out=None, stream=None,
+                      extra_table=None):
+        """(dist [Q,k] fp32, ids [Q,k] int32) on the queries' device.  extra_table:
+        the leaf extra byte's decode table (device fp32 [256]; et_etree_topk_extra)."""
         torch = _t()
         ref = luts if luts is not None else queries
         Q = ref.shape[0]
@@ -202,6 +209,14 @@ class Index:
             dist, ids = out
         nb = self.et_workspace_size(Q, k)
         ws = self._workspace(nb, ref.device, stream)
+        if extra_table is not None:
+            _dev(extra_table, torch.float32)
+            if extra_table.numel() != 256:
+                raise ValueError("extra_table must hold 256 entries")
+            check(_lib.load().et_etree_topk_extra(self._h, _ptr(codebooks), d, _ptr(luts), _ptr(queries), Q, k,
+                                                  _ptr(extra_table), _ptr(dist), _ptr(ids), _ptr(ws), ws.numel(),
+                                                  _stream(stream)))
+            return dist, ids
         check(_lib.load().et_etree_topk(self._h, _ptr(codebooks), d, _ptr(luts), _ptr(queries), Q, k,
                                         _ptr(dist), _ptr(ids), _ptr(ws), ws.numel(), _stream(stream)))
         return dist, ids

@@ -145,6 +145,7 @@ struct et_index {
   bool fused = false;                // forest with M <= 8: one scan over masked tuple records
   et::DevBuf fused_rec;
   et::DevBuf narrow_rec;             // forest with 8 < M <= 16: narrow-scan tuple records (2 x uint4)
+  et::DevBuf group_extra;            // leaf extra byte per group (et_index_set_extra)
   int64_t n_leaves[et::kMaxTrees] = {};
   et::DevBuf group_off, ids, group_mult, group_minid, slot2group;
   et::DevBuf t0_tup_off, tup_leaf[et::kMaxTrees];
@@ -1108,19 +1109,24 @@ et_status et_etree_distances(const et_index* ix, const float* codebooks, int32_t
   ET_API_END
 }
 
-et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, const float* luts,
-                        const float* queries, int64_t Q, int32_t k, float* dist, int32_t* ids, void* workspace,
-                        size_t ws, void* stream) {
-  ET_API_BEGIN
+}  // extern "C"
+
+// et_etree_topk / et_etree_topk_extra (etab: the leaf extra byte's decode
+// table, device [256], or null).
+static void etree_topk_impl(const et_index* ix, const float* codebooks, int32_t d, const float* luts,
+                            const float* queries, int64_t Q, int32_t k, const float* etab, float* dist, int32_t* ids,
+                            void* workspace, size_t ws, void* stream) {
   if (!ix || !dist || !ids) fail(ET_ERR_CONFIG, "null argument");
   if (ix->kind == kIvf) fail(ET_ERR_CONFIG, "use et_ivf_topk for IVF indexes");
   if (k < 1 || k > kTopkMax) fail(ET_ERR_CONFIG, "k must be 1..256");
   if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
-  if (Q == 0) { g_err.clear(); return ET_OK; }
+  if (Q == 0) return;
+  if (etab && (!ix->group_extra.p || ix->T != 1)) fail(ET_ERR_CONFIG, "no leaf extra bytes (et_index_set_extra)");
   ScanParams sp;
   table_source(sp, ix, codebooks, d, luts, queries);
   const int nsm = num_sms();
   Plan pl = make_plan(ix, Q, k, nsm);
+  if (etab && pl.MTmax != 8) fail(ET_ERR_CONFIG, "leaf extra bytes: 8-level trees (M = 8)");
   const size_t need = ws_bytes(ix, pl, Q, false, 1);
   if (!workspace || ws < need) fail(ET_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
   Carve c{reinterpret_cast<char*>(workspace), 0, ws};
@@ -1165,6 +1171,14 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
   // chunk holds <= 8 queries (few queries per SM, c3) -- all 16 levels' tables
   // in shared memory, the tuples scanned once, no per-tree partials or join;
   // same plan, same workspace.  Lists of query slot q: lanes q + 8 g, g < 4.
+  if (etab) {   // leaf extra byte: the 4-stream top-k scan with + E[e] (buffers sized for 4 streams)
+    sp.gextra = ix->group_extra.as<uint8_t>();
+    sp.etab = etab;
+    sp.long_ranges = 0;
+    cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk, extra)");
+    cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
+    return;
+  }
   const bool narrow = ix->narrow_rec.p && !sp.luts && sp.vec4 && narrow_supported(sp.s) && fp.fast &&
                       pl.S == 1 && (Q + pl.n_chunks - 1) / pl.n_chunks <= 8 && !narrow_off();
   if (narrow) {
@@ -1174,13 +1188,51 @@ et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, c
     fp.lgroups = 4;
     cuda_check(timed("scan", st, [&] { return launch_narrow(sp, st); }), "scan(narrow)");
     cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
-    g_err.clear();
-    return ET_OK;
+    return;
   }
   // (a finalize fused into the scan kernel was measured +30 us on c2: its
   // latency-bound tail runs with the SM otherwise idle)
   cuda_check(timed("scan", st, [&] { return launch_scan(sp, pl.MTmax, st); }), "scan(topk)");
   cuda_check(timed("finalize", st, [&] { return launch_finalize(fp, st); }), "finalize");
+}
+
+extern "C" {
+
+et_status et_etree_topk(const et_index* ix, const float* codebooks, int32_t d, const float* luts,
+                        const float* queries, int64_t Q, int32_t k, float* dist, int32_t* ids, void* workspace,
+                        size_t ws, void* stream) {
+  ET_API_BEGIN
+  etree_topk_impl(ix, codebooks, d, luts, queries, Q, k, nullptr, dist, ids, workspace, ws, stream);
+  ET_API_END
+}
+
+et_status et_etree_topk_extra(const et_index* ix, const float* codebooks, int32_t d, const float* luts,
+                              const float* queries, int64_t Q, int32_t k, const float* extra_table, float* dist,
+                              int32_t* ids, void* workspace, size_t ws, void* stream) {
+  ET_API_BEGIN
+  if (!extra_table) fail(ET_ERR_CONFIG, "null extra_table");
+  etree_topk_impl(ix, codebooks, d, luts, queries, Q, k, extra_table, dist, ids, workspace, ws, stream);
+  ET_API_END
+}
+
+et_status et_index_set_extra(et_index* ix, const uint8_t* extra, int64_t n) {
+  ET_API_BEGIN
+  if (!ix || !extra) fail(ET_ERR_CONFIG, "null argument");
+  if (ix->kind != kTree || ix->T != 1) fail(ET_ERR_CONFIG, "leaf extra bytes: single E-Tree indexes only");
+  if (n != ix->N) fail(ET_ERR_DIMENSION, "n != the index's N");
+  if (!ix->slot2group.p) fail(ET_ERR_CONFIG, "index without slot map");
+  std::vector<uint32_t> s2g((size_t)n);
+  cuda_check(cudaMemcpy(s2g.data(), ix->slot2group.p, (size_t)n * 4, cudaMemcpyDeviceToHost), "slot map");
+  std::vector<int> ge((size_t)ix->n_groups, -1);
+  for (int64_t i = 0; i < n; ++i) {   // the byte lives on the leaf: one per distinct code
+    int& g = ge[s2g[(size_t)i]];
+    if (g < 0) g = extra[i];
+    else if (g != extra[i]) fail(ET_ERR_INVALID_CODE, "extra byte differs among vectors with the same code");
+  }
+  std::vector<uint8_t> gb(ge.size());
+  for (size_t j = 0; j < ge.size(); ++j) gb[j] = (uint8_t)std::max(0, ge[j]);
+  ix->group_extra.reset();
+  ix->group_extra.upload(gb);
   ET_API_END
 }
 

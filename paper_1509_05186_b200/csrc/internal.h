@@ -72,6 +72,8 @@ struct ScanParams {
   const float* luts = nullptr;        // [Q][M][K]        (materialised tables) or null
   const float4* cbt = nullptr;        // [M][s/4][K] chunk-major codebook copy (16 < s <= 64) or null
   const uint4* nrec = nullptr;        // narrow forest records, 2 per tuple (narrow.cuh) or null
+  const uint8_t* gextra = nullptr;    // leaf extra byte per group or null
+  const float* etab = nullptr;        // its decode table [256] (device, per call)
   const float* coarse = nullptr;      // [nlist][d]       (IVF residual tables) or null
   const int* layer_sub = nullptr;     // [M] subspace of each code byte (chunk order), device copy
   int lsub[kMaxTrees * kMaxMT] = {};  // the same, by value (kernel parameters: no dependent load)

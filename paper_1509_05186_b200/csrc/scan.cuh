@@ -1367,7 +1367,11 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
 // four shuffles per leaf; a leaf costs (MT - LCP) shared-memory / TMEM
 // lookups (masked records: the levels of its mask), MT - 1 FADDs and a
 // predicated emit.
-template <int MT, bool MASKED, bool TOPK, int NS, int FS>
+// EX: leaf extra byte: the leaf's byte (p.gextra, one per group,
+// loaded with the record batch) indexes the decode table staged in shared
+// memory (sm.bigstage, free after the table build) and its entry is added
+// after the M lookups: dist = (((v0 + v1) + ...) + E[e]) (oracle/leafextra.py).
+template <int MT, bool MASKED, bool TOPK, int NS, int FS, bool EX = false>
 __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b) {
   const ScanParams& p = *e.p;
   const int lane = lane_id();
@@ -1399,9 +1403,16 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
   };
   uint4 nx[NS];
   float v[NS][MT];
+  uint32_t nxe[NS], cure[NS];                        // EX: the leaves' extra bytes (next / current batch)
+  auto load_extra = [&](int k, uint32_t off) -> uint32_t {
+    return (EX && off + lane < sl[k]) ? (uint32_t)__ldg(p.gextra + s0[k] + off + lane) : 0u;
+  };
+  const uint32_t etab_s = smem_u32(sm.bigstage);
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
     nx[k] = load_batch(k, 0);
+    nxe[k] = load_extra(k, 0);
+    cure[k] = 0u;
 #pragma unroll
     for (int l = 0; l < MT; ++l) v[k][l] = 0.f;
   }
@@ -1411,6 +1422,7 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
     for (int k = 0; k < NS; ++k) {
       cur[k] = nx[k];
       nx[k] = load_batch(k, off + 32);
+      if constexpr (EX) { cure[k] = nxe[k]; nxe[k] = load_extra(k, off + 32); }
     }
     const int n = (int)min(32u, steps - off);
     // Generic steps (the range's first leaf: every level looked up; the last
@@ -1467,6 +1479,13 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
 #pragma unroll
           for (int k = 0; k < NS; ++k) dist[k] = dist[k] + v[k][l];
       }
+      if constexpr (EX) {   // + E[e] of the leaf's extra byte (one broadcast LDS per stream)
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const uint32_t ek = __shfl_sync(FULLMASK, cure[k], j);
+          dist[k] = dist[k] + lds(etab_s + (ek << 2));
+        }
+      }
       if constexpr (!TOPK) {
 #pragma unroll
         for (int k = 0; k < NS; ++k)
@@ -1513,9 +1532,13 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
 }
 
 
-template <int MT, bool MASKED, int NS = kStreams>
+template <int MT, bool MASKED, int NS = kStreams, bool EX = false>
 __device__ __forceinline__ void scan_tree3_mode(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a,
                                                 uint32_t b) {
+  if constexpr (EX) {   // leaf extra byte: single trees, top-k (host: et_etree_topk_extra)
+    if constexpr (!MASKED) scan_tree3<MT, false, true, NS, 0, true>(e, sm, tr, a, b);
+    return;
+  }
   // fused forests of two 4-level trees (the c5 split 0-3 | 4-7): the tree
   // boundary at compile time
   if (MASKED && MT == 8 && e.p->fsplit == (1u << 4)) {
@@ -1638,7 +1661,7 @@ __device__ __forceinline__ void scan_any(EmitCtx& e, const SmemScan& sm, const T
 // long leaf ranges, p.long_ranges: more independent chains per warp; short
 // ranges keep kStreams -- a separate instantiation, so neither pays the other's
 // registers or code).
-template <int SS, int MTC, int MODE, int NS = kStreams>
+template <int SS, int MTC, int MODE, int NS = kStreams, bool EX = false>
 __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant__ ScanParams p) {
   constexpr bool FOREST = (MODE == 1);
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1771,6 +1794,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       tmem_fence_after();
     }
     if constexpr (!(SS == kDC && MTC > 0)) phase_mark(unit, t == 0 ? 7 : 5);   // tables of tree t ready
+    if constexpr (EX) {   // the extra byte's decode table -> the (now free) staging area
+      for (int i = threadIdx.x; i < 256; i += kThreads) sm.bigstage[i] = __ldg(p.etab + i);
+      __syncthreads();
+    }
     uint32_t lo = 0, hi = (uint32_t)tr.n_leaves;
     if (t == 0) {
       if (p.chunk_lo) { lo = __ldg(p.chunk_lo + chunk); hi = __ldg(p.chunk_hi + chunk); }
@@ -1787,7 +1814,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       if constexpr (FOREST) {
         scan_any<MTC, 0>(e, sm, tr, wa, wb, lut0g);   // per-leaf partials of every tree
       } else if constexpr (MTC > 0) {
-        scan_tree3_mode<MTC, MODE == 2, NS>(e, sm, tr, wa, wb);
+        scan_tree3_mode<MTC, MODE == 2, NS, EX>(e, sm, tr, wa, wb);
       } else {
         scan2_dispatch<MODE == 2>(e, sm, tr, wa, wb);
       }
@@ -1897,12 +1924,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
 }
 
 
-template <int SS, int MTC, int MODE, int NS = kStreams>
+template <int SS, int MTC, int MODE, int NS = kStreams, bool EX = false>
 static cudaError_t launch_scan_t(const ScanParams& p, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS, MTC, MODE, NS>,
+  cudaError_t e = cudaFuncSetAttribute(scan_kernel<SS, MTC, MODE, NS, EX>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  scan_kernel<SS, MTC, MODE, NS><<<p.n_units, kThreads, smem, st>>>(p);
+  scan_kernel<SS, MTC, MODE, NS, EX><<<p.n_units, kThreads, smem, st>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -1924,6 +1951,12 @@ cudaError_t launch_scan_s(const ScanParams& p, size_t smem, cudaStream_t st) {
                                         : launch_scan_t<SS, 8, 2>(p, smem, st);
     }
     return launch_scan_t<SS, 0, 2>(p, smem, st);
+  }
+  if (p.gextra) {   // leaf extra byte: 8-level single trees, top-k
+    if constexpr (SS == 16 || SS == 0) {
+      if (mt == 8 && p.mode == kModeTopk) return launch_scan_t<SS, 8, 0, kStreams, true>(p, smem, st);
+    }
+    return cudaErrorNotSupported;
   }
   if (mt == 8) return p.long_ranges ? launch_scan_t<SS, 8, 0, kStreamsLong>(p, smem, st)
                                     : launch_scan_t<SS, 8, 0>(p, smem, st);

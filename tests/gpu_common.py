@@ -41,10 +41,12 @@ def oracle_dist(cb, qx_row, codes_sel):
     return pq.adc(pq.lut64(cb, qx_row[None, :]), codes_sel)[0]
 
 
-def check_topk(gd, gi, cb, qx, codes, k, qidx, ids_map=None, rtol=RTOL):
+def check_topk(gd, gi, cb, qx, codes, k, qidx, ids_map=None, rtol=RTOL, full_fn=None):
     """Compare GPU top-k (gd, gi: numpy [Q, k]) with the oracle for queries qidx.
 
     ``ids_map``: slot -> id array when ids are not the slots (None = identity).
+    ``full_fn(q)``: the oracle's distances of query q to every slot (default:
+    ADC64 of the PQ codes).
     """
     N = len(codes)
     ids_all = np.arange(N) if ids_map is None else np.asarray(ids_map)
@@ -53,7 +55,7 @@ def check_topk(gd, gi, cb, qx, codes, k, qidx, ids_map=None, rtol=RTOL):
         inv = np.empty(ids_all.max() + 1, dtype=np.int64)
         inv[ids_all] = np.arange(N)
     for q in qidx:
-        full = oracle_dist(cb, qx[q], codes)
+        full = full_fn(q) if full_fn is not None else oracle_dist(cb, qx[q], codes)
         # the oracle's full sort on the exact superset {distance <= k-th smallest}
         kk = min(k, N)
         kth = np.partition(full, kk - 1)[kk - 1]
