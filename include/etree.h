@@ -171,6 +171,17 @@ et_status et_compute_luts(const float* codebooks, int32_t d, int32_t M, int32_t 
 et_status et_workspace_size(const et_index* index, int64_t Q, int32_t k,
                             int32_t nprobe, size_t* bytes);
 
+/* Inner-product tables (maximum inner product search; "extend ADC
+ * to ... scalar product"; reading A26): luts[q][m][k] =
+ * B[q][m] - <q_m, c_m(k)> with B[q][m] = max_k <q_m, c_m(k)> (fp32, the dot
+ * product as a j-ascending FMA chain), offsets[q] = sum_m B[q][m].  Every entry
+ * is >= 0, so et_etree_topk(luts = these) returns the k largest inner products
+ * <q, x_hat> = offsets[q] - dist.  codebooks [M][K][d/M], queries [Q][d],
+ * luts [Q][M][K], offsets [Q]: DEVICE fp32.  Errors: as et_compute_luts. */
+et_status et_compute_ip_luts(const float* codebooks, int32_t d, int32_t M, int32_t K,
+                             const float* queries, int64_t Q, float* luts, float* offsets,
+                             void* stream);
+
 /* The launch plan et_etree_topk (k > 0) or et_etree_distances (k <= 0) uses
  * for Q queries on the current device: query chunks (one CTA each, <= 32
  * queries), leaf segments per chunk (S) and lockstep leaf streams per scan

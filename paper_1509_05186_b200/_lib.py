@@ -67,6 +67,7 @@ SIGNATURES = [
     ("et_workspace_size", C.c_int, [P, I64, I32, I32, C.POINTER(SZ)]),
     ("et_plan_info", C.c_int, [P, I64, I32, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)]),
     ("et_index_set_extra", C.c_int, [P, P, I64]),
+    ("et_compute_ip_luts", C.c_int, [P, I32, I32, I32, P, I64, P, P, P]),
     ("et_etree_topk_extra", C.c_int, [P, P, I32, P, P, I64, I32, P, P, P, P, SZ, P]),
     ("et_etree_distances", C.c_int, [P, P, I32, P, P, I64, P, P, SZ, P]),
     ("et_etree_topk", C.c_int, [P, P, I32, P, P, I64, I32, P, P, P, SZ, P]),

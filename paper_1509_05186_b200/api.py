@@ -262,6 +262,21 @@ def et_compute_luts(codebooks, queries, stream=None):
     return luts
 
 
+def et_compute_ip_luts(codebooks, queries, stream=None):
+    """(luts [Q,M,K], offsets [Q]): shifted inner-product tables (reading A26);
+    et_etree_topk(luts=luts) then ranks by largest <q, x_hat> = offsets - dist."""
+    torch = _t()
+    _dev(codebooks, torch.float32)
+    _dev(queries, torch.float32)
+    M, K, s = codebooks.shape
+    Q, d = queries.shape
+    luts = torch.empty((Q, M, K), dtype=torch.float32, device=queries.device)
+    off = torch.empty((Q,), dtype=torch.float32, device=queries.device)
+    check(_lib.load().et_compute_ip_luts(_ptr(codebooks), d, M, K, _ptr(queries), Q, _ptr(luts), _ptr(off),
+                                         _stream(stream)))
+    return luts, off
+
+
 def et_encode(codebooks, x, centroids=None, assign=None, stream=None):
     torch = _t()
     _dev(codebooks, torch.float32)

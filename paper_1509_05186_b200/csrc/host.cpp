@@ -1043,6 +1043,20 @@ et_status et_compute_luts(const float* codebooks, int32_t d, int32_t M, int32_t 
   ET_API_END
 }
 
+et_status et_compute_ip_luts(const float* codebooks, int32_t d, int32_t M, int32_t K, const float* queries,
+                             int64_t Q, float* luts, float* offsets, void* stream) {
+  ET_API_BEGIN
+  if (M <= 0 || K <= 0 || K > 256) fail(ET_ERR_CONFIG, "bad M/K");
+  if (d <= 0 || d % M) fail(ET_ERR_SUBSPACE_SPLIT, "d % M != 0");
+  if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
+  if (Q == 0) { g_err.clear(); return ET_OK; }
+  if (!codebooks || !queries || !luts || !offsets) fail(ET_ERR_CONFIG, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  cuda_check(timed("luts", st, [&] { return launch_ip_luts(codebooks, d, M, K, queries, Q, luts, offsets, st); }),
+             "compute_ip_luts");
+  ET_API_END
+}
+
 et_status et_workspace_size(const et_index* ix, int64_t Q, int32_t k, int32_t nprobe, size_t* bytes) {
   ET_API_BEGIN
   if (!ix || !bytes) fail(ET_ERR_CONFIG, "null argument");

@@ -150,6 +150,8 @@ cudaError_t launch_fill_flat(int64_t Q, int n_chunks, int* chunk_q, int* qslot_o
 cudaError_t launch_gather_full(const float* leafdist, const uint32_t* slot2group,
                                int64_t n_groups, int64_t n, const int* qslot, int64_t Q,
                                float* out, cudaStream_t st);
+cudaError_t launch_ip_luts(const float* codebooks, int d, int M, int K, const float* queries, int64_t Q,
+                           float* luts, float* off, cudaStream_t st);
 cudaError_t launch_cb_chunks(const float* codebooks, int M, int K, int s, float4* out, cudaStream_t st);
 cudaError_t launch_luts(const float* codebooks, int d, int M, int K, const float* queries,
                         int64_t Q, float* luts, bool vec4, cudaStream_t st);

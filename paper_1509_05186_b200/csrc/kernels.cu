@@ -846,6 +846,71 @@ cudaError_t launch_luts(const float* codebooks, int d, int M, int K, const float
 }
 
 // ---------------------------------------------------------------------------
+// K1': inner-product tables for maximum inner product search (P:107-108,
+// P:135, reading A26; oracle/ip.py): T[q][m][k] = B[q][m] - <q_m, c_m(k)>,
+// B[q][m] = max_k <q_m, c_m(k)>, off[q] = sum_m B[q][m] (m ascending).  Every
+// entry is >= 0 (B - ip in fp32 with B >= ip), so the E-Tree's smallest table
+// sums -- off[q] - <q, x_hat> -- are the largest inner products.  Block = 8
+// queries, thread = codeword; the dot product is the j-ascending FMA chain.
+// ---------------------------------------------------------------------------
+constexpr int kIpQ = 8;
+
+__global__ void __launch_bounds__(256) ip_lut_kernel(const float* __restrict__ codebooks, int d, int M, int K,
+                                                     const float* __restrict__ queries, int64_t Q,
+                                                     float* __restrict__ luts, float* __restrict__ off) {
+  __shared__ float red[8][kIpQ];
+  __shared__ float bq[kIpQ];
+  const int s = d / M;
+  const int64_t q0 = (int64_t)blockIdx.x * kIpQ;
+  const int nq = (Q - q0 < (int64_t)kIpQ) ? (int)(Q - q0) : kIpQ;
+  const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
+  const bool kv = k < K;
+  float osum = 0.f;                                  // thread i < nq: off of query q0 + i
+  for (int m = 0; m < M; ++m) {
+    const float* c = codebooks + ((size_t)m * K + (kv ? k : 0)) * s;
+    float ip[kIpQ];
+#pragma unroll
+    for (int i = 0; i < kIpQ; ++i) ip[i] = 0.f;
+    for (int j = 0; j < s; ++j) {
+      const float cj = __ldg(c + j);
+#pragma unroll
+      for (int i = 0; i < kIpQ; ++i)
+        if (i < nq) ip[i] = fmaf(__ldg(queries + (size_t)(q0 + i) * d + (size_t)m * s + j), cj, ip[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kIpQ; ++i) {                 // max over the codewords
+      float v = kv ? ip[i] : -FLT_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULLMASK, v, o));
+      if (lane == 0) red[warp][i] = v;
+    }
+    __syncthreads();
+    if (k < kIpQ) {
+      float b = red[0][k];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = fmaxf(b, red[w][k]);
+      bq[k] = b;
+      osum = (m == 0) ? b : osum + b;
+    }
+    __syncthreads();
+    if (kv) {
+#pragma unroll
+      for (int i = 0; i < kIpQ; ++i)
+        if (i < nq) luts[((size_t)(q0 + i) * M + m) * K + k] = bq[i] - ip[i];
+    }
+    __syncthreads();
+  }
+  if (k < nq) off[q0 + k] = osum;
+}
+
+cudaError_t launch_ip_luts(const float* codebooks, int d, int M, int K, const float* queries, int64_t Q,
+                           float* luts, float* off, cudaStream_t st) {
+  if (Q <= 0) return cudaSuccess;
+  ip_lut_kernel<<<(unsigned)((Q + kIpQ - 1) / kIpQ), 256, 0, st>>>(codebooks, d, M, K, queries, Q, luts, off);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // K5: naive ADC (comparison): out[q][i] = sum_m T[q][m][code_i[m]], m ascending
 // ---------------------------------------------------------------------------
 __global__ void flat_adc_kernel(const float* __restrict__ luts, int64_t Q, int M, int K,

@@ -70,3 +70,39 @@ def test_extra_byte_must_be_a_function_of_the_code():
         ix.et_index_set_extra(np.array([1, 1, 2, 0], dtype=np.uint8))
     assert ei.value.status == 5   # ET_ERR_INVALID_CODE
     ix.et_index_set_extra(np.array([1, 1, 1, 0], dtype=np.uint8))
+
+
+# ---------------------------------------------------------------- inner product (reading A26)
+
+def test_inner_product_tables_and_topk():
+    """Shifted inner-product tables (oracle/ip.py) and the E-Tree top-k over
+    them = the largest inner products <q, x_hat>."""
+    from oracle import ip as oip
+    cfg, cb, codes, qx, X = pq_inputs("c1", N=30_000, Q=24, n_train=6_000, iters=4)
+    luts, off = api.et_compute_ip_luts(dev(cb), dev(qx))
+    torch.cuda.synchronize()
+    L, O = luts.cpu().numpy().astype(np.float64), off.cpu().numpy().astype(np.float64)
+    T, off64 = oip.ip_tables(cb, qx)
+    # fp32 error bound of B - <q_m, c>: the two dot products' FMA chains
+    # (<= (s + 2) 2^-24 sum_j |q_j c_j| each) plus the subtraction's rounding
+    M, K, s = cb.shape
+    A = np.stack([np.abs(qx[:, m * s:(m + 1) * s]) @ np.abs(cb[m]).T for m in range(M)], axis=1)   # [Q, M, K]
+    tol = (s + 2) * 2.0 ** -24 * (A + A.max(axis=2, keepdims=True)) + 2.0 ** -23 * np.abs(T)
+    assert np.all(np.abs(L - T) <= tol)
+    assert L.min() >= 0 and np.all(L.min(axis=2) == 0)
+    assert np.allclose(O, off64, rtol=1e-5)
+    ix = api.Index.et_build_etree(codes)
+    d, i = ix.et_etree_topk(30, luts=luts)
+    torch.cuda.synchronize()
+    # the scan over the GPU's own tables: C1/C2 protocol (non-negative sums)
+    check_topk(d.cpu().numpy(), i.cpu().numpy(), None, qx, codes, 30, range(cfg.Q),
+               full_fn=lambda q: pq.adc(L[q:q + 1], codes)[0])
+    # and the ranking is the inner product's: the returned codes' exact <q, x_hat>
+    # are the largest, within the tables' error bound
+    IP = oip.inner_products(cb, qx, codes)
+    gi = i.cpu().numpy()
+    for q in range(cfg.Q):
+        best = np.sort(IP[q])[::-1][:30]
+        got = IP[q][gi[q]]
+        slack = (tol[q].max(axis=1).sum()) * 2
+        assert np.all(np.abs(np.sort(got)[::-1] - best) <= slack)

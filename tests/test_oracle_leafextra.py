@@ -85,3 +85,34 @@ def test_quantize_extra_error_bound_and_range():
     step = E[1] - E[0]
     assert E[0] == 0.0 and e.min() == 0 and e.max() == 255
     assert np.abs(E[e] + shift - v).max() <= step / 2 + 1e-9
+
+
+# ---------------------------------------------------------------- inner product (oracle/ip.py)
+
+from oracle import ip as oip  # noqa: E402
+
+
+def test_ip_tables_shift_identity_and_ranking():
+    """sum_m T = off - <q, x_hat> (brute force on decoded vectors); entries >= 0
+    with a zero per row; smallest sums = largest inner products."""
+    r = np.random.default_rng(7)
+    M, K, s = 4, 8, 3
+    cb = r.normal(size=(M, K, s))
+    codes = r.integers(0, K, size=(200, M)).astype(np.uint8)
+    q = r.normal(size=(5, M * s))
+    T, off = oip.ip_tables(cb, q)
+    assert T.min() >= 0 and np.all(T.min(axis=2) == 0)
+    S = pq.adc(T, codes)
+    IP = oip.inner_products(cb, q, codes)
+    assert np.allclose(off[:, None] - S, IP, rtol=0, atol=1e-12)
+    for i in range(5):
+        assert np.array_equal(np.argsort(S[i], kind="stable")[:10], np.argsort(-IP[i], kind="stable")[:10])
+
+
+def test_ip_of_codeword_concatenation_brute_force():
+    r = np.random.default_rng(8)
+    cb = r.normal(size=(2, 3, 2))
+    codes = np.array([[0, 2], [1, 1]], dtype=np.uint8)
+    q = np.array([[1.0, -2.0, 0.5, 3.0]])
+    want = [q[0] @ np.r_[cb[0][0], cb[1][2]], q[0] @ np.r_[cb[0][1], cb[1][1]]]
+    assert np.allclose(oip.inner_products(cb, q, codes)[0], want)
