@@ -427,7 +427,10 @@ def roofline(cfg, stats, kern_ms, peaks, clock_mhz, Q, n_tables=None, lookups=No
         out = {"bound": "smem", "unit": "Tlookup/s",
                "note": "lookups = (L1+L2+postfix) per table; peak = 148 SM x 32 lookups/clk x sm_max_mhz"}
     out.update({"achieved": round(achieved, 4), "peak": round(peak, 4), "frac": round(achieved / peak, 4),
-                "traffic": None, "kernel": "scan_kernel (fused tables + Distance-Context scan + top-k candidates)",
+                "traffic": None,
+                "kernel": ("narrow_kernel (fused tables of all 16 levels + masked tuple scan + top-k candidates)"
+                           if cfg.forest_split and cfg.M > 8 else
+                           "scan_kernel (fused tables + Distance-Context scan + top-k candidates)"),
                 "alu_ops": ops, "lookups": lk})
     return out
 
@@ -844,7 +847,7 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     kern = {}
-    for name in ("fill", "probe", "bucket", "scan", "finalize", "luts", "gather"):
+    for name in ("fill", "probe", "bucket", "cb_chunks", "scan", "finalize", "luts", "gather"):
         ms, n = api.et_timing_get(name)
         if n:
             kern[name] = ms / n

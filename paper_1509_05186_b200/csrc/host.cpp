@@ -153,6 +153,7 @@ struct et_index {
   et::DevBuf coarse, coarse_t, codebooks;   // IVF ([nlist][d], [d][nlist], [M][K][s])
   std::vector<uint32_t> list_leaf_off;
   et::DevBuf list_leaf_off_d;
+  et::DevBuf cell_order_d;           // IVF cells by list length, longest first (chunk order)
   double lookups_per_query = 0;      // sum over trees (+ tuples) -- planning
 };
 
@@ -644,6 +645,15 @@ static et_index* build_ivf(const uint8_t* codes_in, const int32_t* ids, int64_t 
   tot.scan_lookups = tot.lookups;
   ix->stats[0] = tot;
   ix->list_leaf_off_d.upload(ix->list_leaf_off);
+  {   // chunk order of the scan: longest lists first within each region (their
+      // chunks take longest; started last they would set the kernel's tail)
+    std::vector<int> order(nlist);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return ix->list_leaf_off[a + 1] - ix->list_leaf_off[a] > ix->list_leaf_off[b + 1] - ix->list_leaf_off[b];
+    });
+    ix->cell_order_d.upload(order);
+  }
   ix->coarse.upload_raw(coarse, (size_t)nlist * d * 4);
   {
     std::vector<float> ct((size_t)nlist * d);
@@ -1272,7 +1282,8 @@ et_status et_ivf_topk(const et_index* ix, const float* queries, int64_t Q, int32
                return launch_probe(ix->coarse_t.as<float>(), ix->nlist, ix->d, queries, Q, nprobe, pr, st);
              }), "probe");
   cuda_check(timed("bucket", st, [&] {
-               return launch_ivf_bucket(pr, Q, nprobe, ix->nlist, ix->list_leaf_off_d.as<uint32_t>(), v.cell_cnt,
+               return launch_ivf_bucket(pr, Q, nprobe, ix->nlist, ix->list_leaf_off_d.as<uint32_t>(),
+                                        ix->cell_order_d.as<int>(), v.cell_cnt,
                                         v.pair_pos, v.chunk_off, v.n_chunks, v.chunk_cell, v.chunk_lo, v.chunk_hi,
                                         w.chunk_q, pl.n_chunks, w.qslot_off, w.qslot, st);
              }), "bucket");

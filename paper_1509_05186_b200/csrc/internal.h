@@ -165,7 +165,7 @@ cudaError_t launch_assign(const float* centroids, int nlist, int d, const float*
 cudaError_t launch_probe(const float* centroids_t, int nlist, int d, const float* queries, int64_t Q,
                          int w, int32_t* probes, cudaStream_t st);
 cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist, const uint32_t* list_leaf_off,
-                              int* cell_cnt, int* pair_pos, int* chunk_off, int* n_chunks, int* chunk_cell,
+                              const int* cell_order, int* cell_cnt, int* pair_pos, int* chunk_off, int* n_chunks, int* chunk_cell,
                               uint32_t* chunk_lo, uint32_t* chunk_hi, int* chunk_q, int max_chunks,
                               int* qslot_off, int* qslot, cudaStream_t st);
 cudaError_t launch_merge(const float* in_dist, const int32_t* in_ids, int G, int64_t Q, int k,

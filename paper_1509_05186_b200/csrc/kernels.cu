@@ -1184,7 +1184,8 @@ cudaError_t launch_probe(const float* cT, int nlist, int d, const float* queries
 // probe (rank 0), tier 1 the other probes.  A cell's pairs then form one list
 // -- its tier-0 pairs first -- cut into chunks of 32; every cell's FIRST chunk
 // comes first in the chunk order (region A), the cells' remaining chunks after
-// (region B).  So the scan of a query's nearest list -- where its nearest codes
+// (region B), each region's cells longest list first.  So the scan of a
+// query's nearest list -- where its nearest codes
 // most likely are -- runs in the first waves and leaves a tight k-th distance
 // bound in qthr for the query's other probes, and a cell costs ceil(n / 32)
 // chunk scans rather than one per tier (c4: ~4 -> ~3 per cell).
@@ -1202,6 +1203,7 @@ __global__ void ivf_count_kernel(const int32_t* __restrict__ probes, int64_t P, 
 // first of its remaining chunks (region B); chunk_off[2 nlist] = total.
 __global__ void __launch_bounds__(1024) ivf_chunks_kernel(const int* __restrict__ cell_cnt, int nlist,
                                                           const uint32_t* __restrict__ list_leaf_off,
+                                                          const int* __restrict__ cell_order,
                                                           int* chunk_off, int* n_chunks, int* chunk_cell,
                                                           uint32_t* chunk_lo, uint32_t* chunk_hi) {
   __shared__ int pa[1024], pb[1024];
@@ -1209,7 +1211,8 @@ __global__ void __launch_bounds__(1024) ivf_chunks_kernel(const int* __restrict_
   const int per = (nlist + blockDim.x - 1) / blockDim.x;
   const int c0 = min(nlist, t * per), c1 = min(nlist, c0 + per);
   int la = 0, lb = 0;
-  for (int c = c0; c < c1; ++c) {
+  for (int ci = c0; ci < c1; ++ci) {   // cells in list-length order (longest first)
+    const int c = cell_order[ci];
     const int n = cell_cnt[c] + cell_cnt[nlist + c];
     la += n > 0 ? 1 : 0;
     lb += n > 0 ? ((n + 31) >> 5) - 1 : 0;
@@ -1226,7 +1229,8 @@ __global__ void __launch_bounds__(1024) ivf_chunks_kernel(const int* __restrict_
   }
   const int total_a = pa[blockDim.x - 1];
   int ra = pa[t] - la, rb = total_a + pb[t] - lb;
-  for (int c = c0; c < c1; ++c) {
+  for (int ci = c0; ci < c1; ++ci) {
+    const int c = cell_order[ci];
     const int n = cell_cnt[c] + cell_cnt[nlist + c];
     const int nb = n > 0 ? ((n + 31) >> 5) - 1 : 0;
     chunk_off[c] = n > 0 ? ra : -1;
@@ -1259,7 +1263,7 @@ __global__ void ivf_scatter_kernel(const int32_t* __restrict__ probes, int64_t Q
 }
 
 cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist, const uint32_t* list_leaf_off,
-                              int* cell_cnt, int* pair_pos, int* chunk_off, int* n_chunks, int* chunk_cell,
+                              const int* cell_order, int* cell_cnt, int* pair_pos, int* chunk_off, int* n_chunks, int* chunk_cell,
                               uint32_t* chunk_lo, uint32_t* chunk_hi, int* chunk_q, int max_chunks,
                               int* qslot_off, int* qslot, cudaStream_t st) {
   cudaError_t e;
@@ -1267,7 +1271,7 @@ cudaError_t launch_ivf_bucket(const int32_t* probes, int64_t Q, int w, int nlist
   if ((e = cudaMemsetAsync(chunk_q, 0xff, (size_t)max_chunks * 32 * 4, st)) != cudaSuccess) return e;
   const int64_t P = Q * w;
   ivf_count_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(probes, P, w, nlist, cell_cnt, pair_pos);
-  ivf_chunks_kernel<<<1, 1024, 0, st>>>(cell_cnt, nlist, list_leaf_off, chunk_off, n_chunks, chunk_cell,
+  ivf_chunks_kernel<<<1, 1024, 0, st>>>(cell_cnt, nlist, list_leaf_off, cell_order, chunk_off, n_chunks, chunk_cell,
                                         chunk_lo, chunk_hi);
   const int64_t n = (P > Q + 1) ? P : Q + 1;
   ivf_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(probes, Q, w, nlist, cell_cnt, pair_pos, chunk_off,

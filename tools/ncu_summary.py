@@ -77,7 +77,7 @@ def main():
             rd *= mult.get(units[col["dram__bytes_read.sum"]], 1)
             wr *= mult.get(units[col["dram__bytes_write.sum"]], 1)
             lines.append(f"| dram read+write per launch | {rd + wr:.0f} | byte |")
-            if "scan_kernel" in name:
+            if "scan_kernel" in name or "narrow_kernel" in name:
                 traffic["scan"] = rd + wr
         except (KeyError, ValueError):
             pass
