@@ -789,21 +789,16 @@ cudaError_t launch_gather_full(const float* leafdist, const uint32_t* slot2group
 // codebook row (m, k) dimensions 4 jc .. 4 jc + 3, so a warp's 32 rows of one
 // chunk are one contiguous 512 B load.  Layout only, no arithmetic.
 // ---------------------------------------------------------------------------
-__global__ void cb_chunks_kernel(const float* __restrict__ cb, int M, int K, int s, float4* __restrict__ out) {
+__global__ void __launch_bounds__(256) cb_chunks_kernel(const float* __restrict__ cb, int K, int s,
+                                                        float4* __restrict__ out) {
   const int nch = s / 4;
-  const int64_t n = (int64_t)M * nch * K;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(i % K);
-    const int64_t mj = i / K;
-    const int jc = (int)(mj % nch), m = (int)(mj / nch);
-    out[i] = __ldg(reinterpret_cast<const float4*>(cb + ((size_t)m * K + k) * s) + jc);
-  }
+  const int m = blockIdx.y, jc = blockIdx.x;       // block = (subspace, chunk); thread = codeword
+  for (int k = threadIdx.x; k < K; k += blockDim.x)
+    out[((size_t)m * nch + jc) * K + k] = __ldg(reinterpret_cast<const float4*>(cb + ((size_t)m * K + k) * s) + jc);
 }
 
 cudaError_t launch_cb_chunks(const float* codebooks, int M, int K, int s, float4* out, cudaStream_t st) {
-  const int64_t n = (int64_t)M * (s / 4) * K;
-  const int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
-  cb_chunks_kernel<<<grid, 256, 0, st>>>(codebooks, M, K, s, out);
+  cb_chunks_kernel<<<dim3((unsigned)(s / 4), (unsigned)M), 256, 0, st>>>(codebooks, K, s, out);
   count_launch();
   return cudaGetLastError();
 }
