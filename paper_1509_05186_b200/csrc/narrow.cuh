@@ -32,8 +32,10 @@ struct NarrowSmem {
   static constexpr uint32_t lvl_bytes = (kNarrowQ / 2) * pair_bytes;
   static constexpr uint32_t stage = kNarrowLevels * kNarrowLvlBytes;
   static constexpr uint32_t thr = stage + kNarrowLevels * lvl_bytes;
-  static constexpr uint32_t total = thr + 32u * 4u;
+  static constexpr uint32_t recs = thr + 32u * 4u;        // the tuple records, when they fit
+  static constexpr uint32_t total = recs;                // + 32 B per tuple (kNarrowSmemRecs)
 };
+constexpr int kNarrowSmemRecs = 2048;                    // tuples whose records are staged in smem
 
 // Tables of every level for the CTA's <= 8 queries: rounds of 4 levels, kWPL
 // warps per level, kR codeword rows per lane; the j-ascending packed FADD2 /
@@ -65,7 +67,10 @@ __device__ __forceinline__ void narrow_build(const ScanParams& p, uint32_t base)
         if (d < NCH) c[d][r] = chunk(l, r, d);
   };
   const int rounds = (p.M + 3) / 4;
-  if (active && lw < p.M) prefill(lw);
+  if (active && lw < p.M) prefill(lw);                    // in flight during the staging wait
+  asm volatile("cp.async.wait_all;" ::: "memory");         // this thread's staged copies landed
+  __syncthreads();                                        // everyone's
+  phase_mark((int)blockIdx.x, 1);
   for (int rd = 0; rd < rounds; ++rd) {
     const int l = rd * 4 + lw;
     if (active && l < p.M) {
@@ -123,8 +128,9 @@ __device__ __forceinline__ uint32_t nrec_hw(const uint4 (&r)[2], int l) {
 // The tuples [wa, wb) of this warp: lane group g walks [ga, gb), lane slot ql
 // is query slot ql.  FS = the level where tree 1 starts (compile time) or 0
 // (tree boundaries from p.fsplit at run time).
+// recs_s: the records in shared memory (staged at kernel entry) or 0 (global).
 template <int FS>
-__device__ void narrow_scan(EmitCtx& e, uint32_t base, uint32_t thr_s, uint32_t wa, uint32_t wb) {
+__device__ void narrow_scan(EmitCtx& e, uint32_t base, uint32_t thr_s, uint32_t recs_s, uint32_t wa, uint32_t wb) {
   const ScanParams& p = *e.p;
   const int lane = lane_id();
   const int ql = lane & (kNarrowQ - 1), g = lane / kNarrowQ;
@@ -138,8 +144,14 @@ __device__ void narrow_scan(EmitCtx& e, uint32_t base, uint32_t thr_s, uint32_t 
 #pragma unroll
   for (int l = 0; l < kNarrowLevels; ++l) v[l] = 0.f;
   auto load = [&](uint32_t t, uint4 (&r)[2]) {
-    if (t < gb) { r[0] = __ldg(rec + 2 * (size_t)t); r[1] = __ldg(rec + 2 * (size_t)t + 1); }
-    else { r[0] = make_uint4(0u, 0u, 0u, 0u); r[1] = r[0]; }
+    if (t >= gb) { r[0] = make_uint4(0u, 0u, 0u, 0u); r[1] = r[0]; return; }
+    if (recs_s) {   // broadcast 16-byte shared loads (8 lanes share one tuple)
+      const float4 a = lds4(recs_s + 32u * t), b = lds4(recs_s + 32u * t + 16u);
+      r[0] = make_uint4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(a.z), __float_as_uint(a.w));
+      r[1] = make_uint4(__float_as_uint(b.x), __float_as_uint(b.y), __float_as_uint(b.z), __float_as_uint(b.w));
+    } else {
+      r[0] = __ldg(rec + 2 * (size_t)t); r[1] = __ldg(rec + 2 * (size_t)t + 1);
+    }
   };
   uint4 cur[2], nx[2];
   load(ga, nx);
@@ -216,12 +228,18 @@ __global__ void __launch_bounds__(kThreads, 1) narrow_kernel(const __grid_consta
                          (uint32_t)j * 8u + (uint32_t)(i & 1) * 4u;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
   }
+  // few tuples (c3: 541): every record into shared memory now, in flight
+  // during the table build (the scan then reads them with broadcast LDS)
+  const bool srec = p.n_groups <= kNarrowSmemRecs;
+  if (srec) {
+    const char* src = reinterpret_cast<const char*>(p.nrec);
+    for (int i = threadIdx.x; i < 2 * p.n_groups; i += kThreads)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(base + L::recs + 16u * (uint32_t)i),
+                   "l"(src + 16 * (size_t)i) : "memory");
+  }
   unsigned* thr = reinterpret_cast<unsigned*>(smem_raw + L::thr);
   if (threadIdx.x < 32) thr[lane] = 0x7f800000u;
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
-  phase_mark(unit, 1);
-  narrow_build<SS>(p, base);
+  narrow_build<SS>(p, base);   // (waits for the staged queries after its first codeword loads)
   __syncthreads();
   phase_mark(unit, 5);
 
@@ -239,9 +257,10 @@ __global__ void __launch_bounds__(kThreads, 1) narrow_kernel(const __grid_consta
   e.ts.buf = e.ts.warp_buf + (size_t)lane * kWarps * p.B;
   const uint64_t G = (uint64_t)p.n_groups;
   const uint32_t wa = (uint32_t)((G * warp) / kWarps), wb = (uint32_t)((G * (warp + 1)) / kWarps);
+  const uint32_t recs_s = srec ? base + L::recs : 0u;
   if (wa < wb) {
-    if (p.fsplit == (1u << 8)) narrow_scan<8>(e, base, base + L::thr, wa, wb);
-    else narrow_scan<0>(e, base, base + L::thr, wa, wb);
+    if (p.fsplit == (1u << 8)) narrow_scan<8>(e, base, base + L::thr, recs_s, wa, wb);
+    else narrow_scan<0>(e, base, base + L::thr, recs_s, wa, wb);
   }
   __syncthreads();
   phase_mark(unit, 3);
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) narrow_kernel(const __grid_consta
 
 template <int SS>
 cudaError_t launch_narrow_s(const ScanParams& p, cudaStream_t st) {
-  const size_t smem = NarrowSmem<SS>::total;
+  const size_t smem = NarrowSmem<SS>::total + (p.n_groups <= kNarrowSmemRecs ? 32u * (size_t)p.n_groups : 0u);
   cudaError_t e = cudaFuncSetAttribute(narrow_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   narrow_kernel<SS><<<p.n_units, kThreads, smem, st>>>(p);
