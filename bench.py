@@ -860,13 +860,9 @@ def run_ours(args):
     dh = torch.empty(out_shape, dtype=torch.float32).pin_memory()
     ih = torch.empty(out_shape if not full else (1, 1), dtype=torch.int32).pin_memory()
     q_stage = torch.empty_like(qd)
-    e_evs = [(ev(), ev()) for _ in range(max(5, args.steps // 4))]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for a, b in e_evs:
-        flush.fill_(1.0)
-        a.record()
+    n_e = max(5, args.steps // 4)
+
+    def serial_once():
         q_stage.copy_(qh, non_blocking=True)
         r = local_step(q_stage)
         if full:
@@ -880,9 +876,45 @@ def run_ours(args):
             if rank == 0 or not merged:   # the merged result is read back once (rank 0)
                 dh.copy_(md, non_blocking=True)
                 ih.copy_(mi, non_blocking=True)
-        b.record()
+
+    # the library's host-buffer call (et_etree_topk_host): uploads, search and
+    # read-backs pipelined in batches on two copy streams + the compute stream;
+    # timed interleaved with the serial one-stream sequence (the host link's
+    # copy rate drifts between runs on this pool, so the two see the same link)
+    use_host = ix is not None and not full and not ivf and not merged
+
+    def host_once():
+        ix.et_etree_topk_host(k, qh, cbd, out=(dh, ih), n_batches=args.host_batches)
+
+    if use_host:
+        for _ in range(2):
+            host_once()
+    e_evs = [(ev(), ev()) for _ in range(n_e)]
+    p_evs = [(ev(), ev()) for _ in range(n_e)]
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
-    e2e_ms = comm.allmax(sum(a.elapsed_time(b) for a, b in e_evs) / len(e_evs))
+    for (a, b), (c, d) in zip(e_evs, p_evs):
+        flush.fill_(1.0)
+        a.record()
+        serial_once()
+        b.record()
+        if use_host:
+            flush.fill_(1.0)
+            c.record()
+            host_once()
+            d.record()
+    torch.cuda.synchronize()
+    e2e_ms = comm.allmax(sum(a.elapsed_time(b) for a, b in e_evs) / n_e)
+    e2e_how = "serial: H2D copy, step, D2H copy on one stream"
+    e2e_serial_ms = None
+    if use_host:
+        if world == 1:   # the host outputs equal the device step's (same queries, same kernels)
+            assert torch.equal(dh, dist_out.cpu()) and torch.equal(ih, ids_out.cpu()), "host-buffer call differs"
+        e2e_serial_ms = e2e_ms
+        e2e_ms = comm.allmax(sum(c.elapsed_time(d) for c, d in p_evs) / n_e)
+        e2e_how = (f"et_etree_topk_host: pinned host queries in, host top-k out, "
+                   f"{api.et_host_batches(Ql, args.host_batches)} batches pipelined (copies on two copy streams)")
     h2d = int(comm.allsum(np.array([qh.numel() * 4], np.int64))[0])
     d2h_mine = dh.numel() * 4 + (0 if full else ih.numel() * 4) if (rank == 0 or not merged) else 0
     d2h = int(comm.allsum(np.array([d2h_mine], np.int64))[0])
@@ -971,7 +1003,8 @@ def run_ours(args):
             "kernels_ms": {k_: round(v, 5) for k_, v in kern.items()},
             "dominant_kernel": dom,
             "e2e": {"value": pairs / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "how": e2e_how,
+                    "serial_ms_per_step": e2e_serial_ms},
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clk.summary(),
             "tree_stats": [{kk_: s[kk_] for kk_ in ("L1", "L2", "total_postfix", "lookups", "paper_bytes")}
@@ -1107,6 +1140,8 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-flat", action="store_true", help="skip the same-box naive-ADC (flat index) arm")
     ap.add_argument("--parity-queries", type=int, default=16)
+    ap.add_argument("--host-batches", type=int, default=0,
+                    help="batches of the e2e host-buffer call (0: the library default)")
     ap.add_argument("--dry-run", default=None, help="module[:attr] of a CPU test backend (tests/)")
     ap.add_argument("--dry-n", type=int, default=20_000)
     ap.add_argument("--dry-q", type=int, default=8)

@@ -213,6 +213,32 @@ et_status et_etree_topk(const et_index* index, const float* codebooks, int32_t d
                         int32_t k, float* dist, int32_t* ids, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* et_etree_topk from HOST buffers (the end-to-end call; north_star item 4's
+ * top-k with the queries' upload and the results' read-back pipelined):
+ * the Q queries are split into n_batches contiguous batches
+ * (n_batches <= 0: et_host_batches' default, >= 16 queries per SM per batch,
+ * at most 8); batch b's queries are copied host -> device on a library copy
+ * stream while batch b - 1 is searched on `stream` (table build, scan and
+ * finalize exactly as et_etree_topk, whose results it returns bit for bit:
+ * the per-query arithmetic does not depend on the batch) and batch b - 2's
+ * results are copied device -> host on a second copy stream.
+ * queries_host: HOST fp32 [Q][d] (page-locked for the copies to overlap);
+ * dist_host / ids_host: HOST fp32 / int32 [Q][k]; queries_dev: DEVICE fp32
+ * [Q][d] staging; dist_dev / ids_dev: DEVICE [Q][k] staging (all caller-owned,
+ * none may be touched until `stream` has passed the call); codebooks: DEVICE
+ * (the index's, as et_etree_topk).  workspace: et_workspace_size of the
+ * largest batch, ceil(Q / n_batches) queries.  Asynchronous: the host
+ * outputs are complete once `stream` reaches the point after the call (the
+ * call makes `stream` wait for the last copy).  The copy streams and events
+ * are per host thread and device.  Errors: as et_etree_topk (checked before
+ * anything is enqueued), ET_ERR_DIMENSION (d <= 0). */
+et_status et_host_batches(int64_t Q, int32_t n_batches, int32_t* out);
+et_status et_etree_topk_host(const et_index* index, const float* codebooks, int32_t d,
+                             const float* queries_host, int64_t Q, int32_t k,
+                             float* dist_host, int32_t* ids_host, int32_t n_batches,
+                             float* queries_dev, float* dist_dev, int32_t* ids_dev,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
 /* Leaf extra byte ("we quantized on the extra information to 1
  * Byte ... and store the extra information on the leaf node"; for Additive
  * Quantization it is Eq. 1's non-zero third term).

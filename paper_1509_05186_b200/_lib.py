@@ -71,6 +71,8 @@ SIGNATURES = [
     ("et_etree_topk_extra", C.c_int, [P, P, I32, P, P, I64, I32, P, P, P, P, SZ, P]),
     ("et_etree_distances", C.c_int, [P, P, I32, P, P, I64, P, P, SZ, P]),
     ("et_etree_topk", C.c_int, [P, P, I32, P, P, I64, I32, P, P, P, SZ, P]),
+    ("et_host_batches", C.c_int, [I64, I32, C.POINTER(I32)]),
+    ("et_etree_topk_host", C.c_int, [P, P, I32, P, I64, I32, P, P, I32, P, P, P, P, SZ, P]),
     ("et_ivf_topk", C.c_int, [P, P, I64, I32, I32, P, P, P, P, SZ, P]),
     ("et_merge_topk", C.c_int, [P, P, I32, I64, I32, P, P, P]),
     ("et_flat_adc", C.c_int, [P, I64, I32, I32, P, I64, P, P]),

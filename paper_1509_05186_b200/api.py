@@ -56,6 +56,13 @@ def version() -> str:
     return _lib.load().et_version().decode()
 
 
+def et_host_batches(Q: int, n_batches: int = 0) -> int:
+    """Batches et_etree_topk_host uses for Q queries (n_batches <= 0: the default)."""
+    out = C.c_int32()
+    check(_lib.load().et_host_batches(Q, n_batches, C.byref(out)))
+    return out.value
+
+
 def et_launch_count() -> int:
     return int(_lib.load().et_launch_count())
 
@@ -220,6 +227,46 @@ class Index:
         check(_lib.load().et_etree_topk(self._h, _ptr(codebooks), d, _ptr(luts), _ptr(queries), Q, k,
                                         _ptr(dist), _ptr(ids), _ptr(ws), ws.numel(), _stream(stream)))
         return dist, ids
+
+    def et_etree_topk_host(self, k: int, queries_host, codebooks, out=None, n_batches: int = 0, stream=None):
+        """et_etree_topk from host buffers (etree.h et_etree_topk_host): queries_host
+        is a CPU fp32 [Q, d] tensor (pinned for the copies to overlap the search);
+        returns host (dist [Q,k] fp32, ids [Q,k] int32), complete once ``stream``
+        (default: the current stream) passes the call.  Device staging buffers
+        are cached per (device, stream, shape)."""
+        torch = _t()
+        if queries_host.is_cuda or not queries_host.is_contiguous() or queries_host.dtype != torch.float32:
+            raise ValueError("queries_host must be a contiguous CPU float32 tensor")
+        _dev(codebooks, torch.float32)
+        Q, d = queries_host.shape
+        dev = codebooks.device
+        if out is None:
+            dist_h = torch.empty((Q, k), dtype=torch.float32).pin_memory()
+            ids_h = torch.empty((Q, k), dtype=torch.int32).pin_memory()
+        else:
+            dist_h, ids_h = out
+            for t, dt in ((dist_h, torch.float32), (ids_h, torch.int32)):
+                if t.is_cuda or not t.is_contiguous() or t.dtype != dt or tuple(t.shape) != (Q, k):
+                    raise ValueError(f"host outputs must be contiguous CPU {dt} tensors of shape {(Q, k)}")
+        nbat = C.c_int32()
+        check(_lib.load().et_host_batches(Q, n_batches, C.byref(nbat)))
+        qmax = -(-Q // max(1, nbat.value))
+        nb = self.et_workspace_size(qmax, k)
+        ws = self._workspace(nb, dev, stream)
+        s = torch.cuda.current_stream(dev) if stream is None else stream
+        key = ("host", dev, s.cuda_stream, Q, d, k)
+        stg = self._ws.get(key)
+        if stg is None:
+            with torch.cuda.stream(s):
+                stg = (torch.empty((Q, d), dtype=torch.float32, device=dev),
+                       torch.empty((Q, k), dtype=torch.float32, device=dev),
+                       torch.empty((Q, k), dtype=torch.int32, device=dev))
+            self._ws[key] = stg
+        qd, dd, idd = stg
+        check(_lib.load().et_etree_topk_host(self._h, _ptr(codebooks), d, _ptr(queries_host), Q, k, _ptr(dist_h),
+                                             _ptr(ids_h), nbat.value, _ptr(qd), _ptr(dd), _ptr(idd), _ptr(ws),
+                                             ws.numel(), _stream(stream)))
+        return dist_h, ids_h
 
     def et_etree_distances(self, queries=None, codebooks=None, luts=None, out=None, stream=None):
         """Full output [Q, N] fp32 indexed by slot."""

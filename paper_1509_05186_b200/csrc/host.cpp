@@ -944,6 +944,8 @@ using namespace et;
   g_err.clear();                                                \
   return ET_OK;
 
+static void host_graphs_forget(const et_index* ix);   // et_etree_topk_host's graph cache
+
 extern "C" {
 
 const char* et_last_error(void) { return g_err.c_str(); }
@@ -1037,7 +1039,10 @@ et_status et_index_info(const et_index* ix, int32_t* T, int64_t* n, int32_t* M, 
   ET_API_END
 }
 
-void et_index_free(et_index* ix) { delete ix; }
+void et_index_free(et_index* ix) {
+  host_graphs_forget(ix);
+  delete ix;
+}
 
 et_status et_compute_luts(const float* codebooks, int32_t d, int32_t M, int32_t K, const float* queries,
                           int64_t Q, float* luts, void* stream) {
@@ -1236,6 +1241,198 @@ et_status et_etree_topk_extra(const et_index* ix, const float* codebooks, int32_
   ET_API_BEGIN
   if (!extra_table) fail(ET_ERR_CONFIG, "null extra_table");
   etree_topk_impl(ix, codebooks, d, luts, queries, Q, k, extra_table, dist, ids, workspace, ws, stream);
+  ET_API_END
+}
+
+}  // extern "C"
+
+// et_etree_topk_host: the host->device copy of batch b + 1 and the
+// device->host copy of batch b - 1 run on two copy streams (one per copy
+// engine) while batch b is searched on the compute stream.  Per host thread
+// and device: the two copy streams, a capture stream and an event pool,
+// created on first use.  With page-locked host buffers the whole sequence is
+// captured once into a CUDA graph per argument set (every pointer and size)
+// and replayed by later calls: one cudaGraphLaunch instead of ~10 host
+// launches per batch (the host enqueue otherwise exceeds the GPU time of a
+// batch).
+namespace {
+struct HostPipe {
+  cudaStream_t h2d = nullptr, d2h = nullptr, cap = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+thread_local std::map<int, HostPipe> t_pipes;
+
+HostPipe& host_pipe(size_t nev) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  HostPipe& hp = t_pipes[dev];
+  if (!hp.h2d) {
+    cuda_check(cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking), "copy stream");
+    cuda_check(cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking), "copy stream");
+    cuda_check(cudaStreamCreateWithFlags(&hp.cap, cudaStreamNonBlocking), "capture stream");
+  }
+  while (hp.ev.size() < nev) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    hp.ev.push_back(e);
+  }
+  return hp;
+}
+
+struct HostArgs {
+  const et_index* ix;
+  const float* codebooks;
+  int32_t d;
+  const float* qh;
+  int64_t Q;
+  int32_t k;
+  float* dh;
+  int32_t* ih;
+  int32_t nb;
+  float* qd;
+  float* dd;
+  int32_t* idd;
+  void* ws;
+  size_t wsb;
+};
+
+// the pipelined sequence on compute stream st (eager, or into a capture)
+void enqueue_host_pipeline(const HostArgs& a, cudaStream_t st) {
+  HostPipe& hp = host_pipe((size_t)2 * a.nb + 2);
+  cudaEvent_t ev_start = hp.ev[2 * a.nb], ev_done = hp.ev[2 * a.nb + 1];
+  // the copies start after the earlier work on st (previous users of the
+  // staging buffers)
+  cuda_check(cudaEventRecord(ev_start, st), "event record");
+  cuda_check(cudaStreamWaitEvent(hp.h2d, ev_start, 0), "stream wait");
+  cuda_check(cudaStreamWaitEvent(hp.d2h, ev_start, 0), "stream wait");
+  const size_t qrow = (size_t)a.d * 4, krow = (size_t)a.k * 4;
+  for (int32_t b = 0; b < a.nb; ++b) {
+    const int64_t q0 = a.Q * b / a.nb, q1 = a.Q * (b + 1) / a.nb, Qb = q1 - q0;
+    cudaEvent_t ev_in = hp.ev[2 * b], ev_out = hp.ev[2 * b + 1];
+    cuda_check(cudaMemcpyAsync(a.qd + (size_t)q0 * a.d, a.qh + (size_t)q0 * a.d, (size_t)Qb * qrow,
+                               cudaMemcpyHostToDevice, hp.h2d), "copy queries");
+    cuda_check(cudaEventRecord(ev_in, hp.h2d), "event record");
+    cuda_check(cudaStreamWaitEvent(st, ev_in, 0), "stream wait");
+    etree_topk_impl(a.ix, a.codebooks, a.d, nullptr, a.qd + (size_t)q0 * a.d, Qb, a.k, nullptr,
+                    a.dd + (size_t)q0 * a.k, a.idd + (size_t)q0 * a.k, a.ws, a.wsb, st);
+    cuda_check(cudaEventRecord(ev_out, st), "event record");
+    cuda_check(cudaStreamWaitEvent(hp.d2h, ev_out, 0), "stream wait");
+    cuda_check(cudaMemcpyAsync(a.dh + (size_t)q0 * a.k, a.dd + (size_t)q0 * a.k, (size_t)Qb * krow,
+                               cudaMemcpyDeviceToHost, hp.d2h), "copy distances");
+    cuda_check(cudaMemcpyAsync(a.ih + (size_t)q0 * a.k, a.idd + (size_t)q0 * a.k, (size_t)Qb * krow,
+                               cudaMemcpyDeviceToHost, hp.d2h), "copy ids");
+  }
+  // st completes only after the last result reached the host
+  cuda_check(cudaEventRecord(ev_done, hp.d2h), "event record");
+  cuda_check(cudaStreamWaitEvent(st, ev_done, 0), "stream wait");
+}
+
+bool page_locked(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeHost;
+}
+
+std::mutex g_hgmu;
+std::map<std::vector<uint64_t>, cudaGraphExec_t> g_host_graphs;   // key[0] = the index
+}  // namespace
+
+// et_index_free: drop the graphs that reference the index
+static void host_graphs_forget(const et_index* ix) {
+  std::lock_guard<std::mutex> lk(g_hgmu);
+  for (auto it = g_host_graphs.begin(); it != g_host_graphs.end();) {
+    if (it->first[0] == (uint64_t)(uintptr_t)ix) { cudaGraphExecDestroy(it->second); it = g_host_graphs.erase(it); }
+    else ++it;
+  }
+}
+
+constexpr int kHostBatchesMax = 64;
+constexpr size_t kHostGraphsMax = 32;
+
+static int32_t host_batches(int64_t Q, int32_t n_batches) {
+  // default: batches of >= 16 queries per SM (one full wave of chunks each),
+  // at most 8
+  int64_t nb = n_batches > 0 ? n_batches : std::min<int64_t>(8, std::max<int64_t>(1, Q / ((int64_t)num_sms() * 16)));
+  nb = std::min<int64_t>(nb, std::min<int64_t>(Q, kHostBatchesMax));
+  return (int32_t)std::max<int64_t>(nb, 1);
+}
+
+extern "C" {
+
+et_status et_host_batches(int64_t Q, int32_t n_batches, int32_t* out) {
+  ET_API_BEGIN
+  if (!out) fail(ET_ERR_CONFIG, "null argument");
+  if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
+  *out = host_batches(Q, n_batches);
+  ET_API_END
+}
+
+et_status et_etree_topk_host(const et_index* ix, const float* codebooks, int32_t d, const float* queries_host,
+                             int64_t Q, int32_t k, float* dist_host, int32_t* ids_host, int32_t n_batches,
+                             float* queries_dev, float* dist_dev, int32_t* ids_dev, void* workspace, size_t ws,
+                             void* stream) {
+  ET_API_BEGIN
+  if (!ix || !codebooks || !queries_host || !dist_host || !ids_host || !queries_dev || !dist_dev || !ids_dev)
+    fail(ET_ERR_CONFIG, "null argument");
+  if (ix->kind == kIvf) fail(ET_ERR_CONFIG, "use et_ivf_topk for IVF indexes");
+  if (k < 1 || k > kTopkMax) fail(ET_ERR_CONFIG, "k must be 1..256");
+  if (Q < 0) fail(ET_ERR_CONFIG, "Q < 0");
+  if (d <= 0) fail(ET_ERR_DIMENSION, "d <= 0");
+  if (Q == 0) { g_err.clear(); return ET_OK; }
+  const int32_t nb = host_batches(Q, n_batches);
+  {  // the largest batch's workspace, checked before anything is enqueued
+    const int64_t qmax = (Q + nb - 1) / nb;
+    const Plan pl = make_plan(ix, qmax, k, num_sms());
+    const size_t need = ws_bytes(ix, pl, qmax, false, 1);
+    if (!workspace || ws < need) fail(ET_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need));
+  }
+  const HostArgs a{ix, codebooks, d, queries_host, Q, k, dist_host, ids_host, nb,
+                   queries_dev, dist_dev, ids_dev, workspace, ws};
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool graph = !g_timing.load() && page_locked(queries_host) && page_locked(dist_host) &&
+                     page_locked(ids_host) && !getenv("ET_HOST_EAGER");
+  if (!graph) {
+    enqueue_host_pipeline(a, st);
+    g_err.clear();
+    return ET_OK;
+  }
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  const std::vector<uint64_t> key{(uint64_t)(uintptr_t)ix, (uint64_t)(uintptr_t)codebooks, (uint64_t)d,
+                                  (uint64_t)(uintptr_t)queries_host, (uint64_t)Q, (uint64_t)k,
+                                  (uint64_t)(uintptr_t)dist_host, (uint64_t)(uintptr_t)ids_host, (uint64_t)nb,
+                                  (uint64_t)(uintptr_t)queries_dev, (uint64_t)(uintptr_t)dist_dev,
+                                  (uint64_t)(uintptr_t)ids_dev, (uint64_t)(uintptr_t)workspace, (uint64_t)ws,
+                                  (uint64_t)dev};
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_hgmu);
+    auto it = g_host_graphs.find(key);
+    if (it != g_host_graphs.end()) exec = it->second;
+  }
+  if (!exec) {
+    HostPipe& hp = host_pipe((size_t)2 * nb + 2);
+    cuda_check(cudaStreamBeginCapture(hp.cap, cudaStreamCaptureModeRelaxed), "begin capture");
+    cudaGraph_t g = nullptr;
+    try {
+      enqueue_host_pipeline(a, hp.cap);
+    } catch (...) {
+      cudaStreamEndCapture(hp.cap, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cuda_check(cudaStreamEndCapture(hp.cap, &g), "end capture");
+    const cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    cuda_check(e, "graph instantiate");
+    std::lock_guard<std::mutex> lk(g_hgmu);
+    if (g_host_graphs.size() >= kHostGraphsMax) {
+      for (auto& kv : g_host_graphs) cudaGraphExecDestroy(kv.second);
+      g_host_graphs.clear();
+    }
+    g_host_graphs[key] = exec;
+  }
+  cuda_check(cudaGraphLaunch(exec, st), "graph launch");
   ET_API_END
 }
 
