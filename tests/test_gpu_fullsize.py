@@ -7,7 +7,8 @@ bench.py times, on sampled outputs:
   the oracle cannot encode 10^8 vectors in test time, so the codes come from
   et_encode (reading C4b in DESIGN.md §3) -- pinned here against the oracle's
   encode on four random 65,536-vector blocks -- and the oracle computes the
-  exact top-k over all 10^8 codes for three sampled queries.
+  exact top-k over all 10^8 codes for three sampled queries; every query's
+  returned pairs and a 4096-code sample bound against ADC64.
 
 Slow (minutes): generation of the 10^8 base vectors dominates.
 """
@@ -118,6 +119,22 @@ def test_c5_full_size_topk_sampled(c5_full):
         mism = g_i != oi
         if mism.any():
             assert np.all(np.abs(truth[mism] - od[mism]) <= RTOL * od[mism]), q
+    # every query (properties that hold at any size): each returned distance is
+    # the oracle's ADC64 of (query, codes[returned id]), ids are distinct, and
+    # no code of a random 4096-code sample beats the k-th returned distance
+    # unless it is in the list (it would belong to the exact top-k).
+    table = pq.lut64(cb, qx)
+    rng = np.random.default_rng(55)
+    samp = np.sort(rng.choice(cfg.N, 4096, replace=False))
+    dsamp = pq.adc(table, codes[samp])                      # [Q, 4096] fp64
+    for q in range(cfg.Q):
+        g_i = gi[q].astype(np.int64)
+        assert len(np.unique(g_i)) == cfg.topk, q
+        truth = pq.adc(table[q:q + 1], codes[g_i])[0]
+        g_d = gd[q].astype(np.float64)
+        assert np.all(np.abs(g_d - truth) <= RTOL * np.maximum(truth, 1e-30)), q
+        better = samp[dsamp[q] < g_d[-1] * (1 - RTOL)]
+        assert np.isin(better, g_i).all(), q
 
 
 # --------------------------------------------------------------------------- c4 at full size
