@@ -124,13 +124,18 @@ struct ScanParams {
 // 2..7 in six 32 KB regions, and stage the chunk's query sub-vectors of all 8
 // levels in their own area; shorter trees keep every level in shared memory.
 constexpr int kTmemLevels = 2;             // levels of an 8-level tree held in TMEM
+#ifndef ET_REC_SMEM
+#define ET_REC_SMEM 0                      // 1: leaf records broadcast through shared memory (scan_tree3 RS)
+#endif
+// RS: kWarps x kStreamsLong x 32 records x 16 B = 24 KB, the 16 KB staging area + this extension
+constexpr uint32_t kRecExtra = ET_REC_SMEM ? (uint32_t)(kWarps * kStreamsLong * 512 - 8 * 16 * 128) : 0u;
 struct ScanSmem { uint32_t levels, big_stage, thr, qidx, stage, tmem_slot, total; };
 __host__ __device__ inline ScanSmem scan_smem(int MTmax) {
   ScanSmem L{};
   L.levels = (MTmax == 8) ? 8 - kTmemLevels : (uint32_t)MTmax;
   uint32_t off = L.levels * 32768u;
   L.big_stage = off;
-  if (MTmax == 8) off += 8u * 16u * 128u;   // [level][query pair][dim][2] fp32
+  if (MTmax == 8) off += 8u * 16u * 128u + kRecExtra;   // [level][query pair][dim][2] fp32 (+ the RS records)
   L.thr = off; off += 128u;
   L.qidx = off; off += 128u;
   L.stage = off; off += 32u * 16u * 4u;

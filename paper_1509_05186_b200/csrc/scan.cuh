@@ -45,6 +45,17 @@ __device__ __forceinline__ float4 lds4(uint32_t a) {
   return v;
 }
 // predicated load: v is returned unchanged when !pred (no shared-memory traffic)
+// leaf-record staging (ET_REC_SMEM): a warp's batch of 32 records per stream in
+// shared memory, read back by every lane at a warp-uniform address (one
+// broadcast LDS.128 per leaf instead of four shuffles)
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u4(uint32_t a, const uint4& v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 __device__ __forceinline__ float lds_if(uint32_t a, bool pred, float v) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.f32 %0, [%1];\n\t}"
                : "+f"(v) : "r"(a), "r"((int)pred));
@@ -1371,7 +1382,10 @@ __device__ void scan_tree(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uin
 // loaded with the record batch) indexes the decode table staged in shared
 // memory (sm.bigstage, free after the table build) and its entry is added
 // after the M lookups: dist = (((v0 + v1) + ...) + E[e]) (oracle/leafextra.py).
-template <int MT, bool MASKED, bool TOPK, int NS, int FS, bool EX = false>
+// RS (ET_REC_SMEM builds, 8-level trees of the fused-build kernel): the batch's
+// records go through the warp's slice of the staging area (sm.bigstage, free
+// after the table build) instead of shuffles.
+template <int MT, bool MASKED, bool TOPK, int NS, int FS, bool EX = false, bool RS = false>
 __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a, uint32_t b) {
   const ScanParams& p = *e.p;
   const int lane = lane_id();
@@ -1408,6 +1422,7 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
     return (EX && off + lane < sl[k]) ? (uint32_t)__ldg(p.gextra + s0[k] + off + lane) : 0u;
   };
   const uint32_t etab_s = smem_u32(sm.bigstage);
+  const uint32_t rs_s = smem_u32(sm.bigstage) + (uint32_t)warp_id() * (uint32_t)(NS * 512);
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
     nx[k] = load_batch(k, 0);
@@ -1424,6 +1439,12 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
       nx[k] = load_batch(k, off + 32);
       if constexpr (EX) { cure[k] = nxe[k]; nxe[k] = load_extra(k, off + 32); }
     }
+    if constexpr (RS) {
+      __syncwarp();                                  // the previous batch's reads are done
+#pragma unroll
+      for (int k = 0; k < NS; ++k) sts_u4(rs_s + (uint32_t)(k * 512) + ((uint32_t)lane << 4), cur[k]);
+      __syncwarp();
+    }
     const int n = (int)min(32u, steps - off);
     // Generic steps (the range's first leaf: every level looked up; the last
     // step: the shorter streams are done) test per stream; all other steps
@@ -1436,7 +1457,8 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
       uint32_t t0[NS], t1[NS];                       // TMEM levels: every stream's reads, one wait
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        rr[k] = shfl_rec(cur[k], j);
+        if constexpr (RS) rr[k] = lds_u4(rs_s + (uint32_t)(k * 512) + ((uint32_t)j << 4));
+        else rr[k] = shfl_rec(cur[k], j);
         t0[k] = t1[k] = 0u;
         if constexpr (lv0_of(MT) == 2) tmem_rec_ld(tq, rr[k], t0[k], t1[k]);
       }
@@ -1532,7 +1554,7 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
 }
 
 
-template <int MT, bool MASKED, int NS = kStreams, bool EX = false>
+template <int MT, bool MASKED, int NS = kStreams, bool EX = false, bool RS = false>
 __device__ __forceinline__ void scan_tree3_mode(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, uint32_t a,
                                                 uint32_t b) {
   if constexpr (EX) {   // leaf extra byte: single trees, top-k (host: et_etree_topk_extra)
@@ -1542,12 +1564,12 @@ __device__ __forceinline__ void scan_tree3_mode(EmitCtx& e, const SmemScan& sm, 
   // fused forests of two 4-level trees (the c5 split 0-3 | 4-7): the tree
   // boundary at compile time
   if (MASKED && MT == 8 && e.p->fsplit == (1u << 4)) {
-    if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, NS, 4>(e, sm, tr, a, b);
-    else scan_tree3<MT, MASKED, false, kStreams, 4>(e, sm, tr, a, b);
+    if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, NS, 4, false, RS>(e, sm, tr, a, b);
+    else scan_tree3<MT, MASKED, false, kStreams, 4, false, RS>(e, sm, tr, a, b);
     return;
   }
-  if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, NS, 0>(e, sm, tr, a, b);
-  else scan_tree3<MT, MASKED, false, kStreams, 0>(e, sm, tr, a, b);
+  if (e.p->mode == kModeTopk) scan_tree3<MT, MASKED, true, NS, 0, false, RS>(e, sm, tr, a, b);
+  else scan_tree3<MT, MASKED, false, kStreams, 0, false, RS>(e, sm, tr, a, b);
 }
 
 template <bool MASKED>
@@ -1814,7 +1836,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(const __grid_constant
       if constexpr (FOREST) {
         scan_any<MTC, 0>(e, sm, tr, wa, wb, lut0g);   // per-leaf partials of every tree
       } else if constexpr (MTC > 0) {
-        scan_tree3_mode<MTC, MODE == 2, NS, EX>(e, sm, tr, wa, wb);
+        // (ET_REC_SMEM: 16-dim fused build only -- its staging area is free during the scan)
+        constexpr bool kRS = (ET_REC_SMEM != 0) && SS == kDC && MTC == 8 && !EX;
+        scan_tree3_mode<MTC, MODE == 2, NS, EX, kRS>(e, sm, tr, wa, wb);
       } else {
         scan2_dispatch<MODE == 2>(e, sm, tr, wa, wb);
       }

@@ -2,7 +2,7 @@
 bench.py times, on sampled outputs:
 
 * c3 -- E-Forest at d = 960 (N = 10^6, Q = 10^3, T = 2, top-100): oracle
-  codebooks and codes; 24 sampled queries against the oracle's exact top-k.
+  codebooks (shortened training) and codes; 24 sampled queries against the oracle's exact top-k.
 * c5 -- E-Forest at N = 10^8 (T = 2 over bytes 0-3 | 4-7, Q = 10^4, top-100):
   the oracle cannot encode 10^8 vectors in test time, so the codes come from
   et_encode (reading C4b in DESIGN.md §3) -- pinned here against the oracle's
@@ -44,7 +44,10 @@ def dev(a):
 
 
 def test_c3_full_size_topk_sampled():
-    cfg, cb, codes, qx, X = pq_inputs("c3")
+    # (the oracle's k-means on 20,000 training vectors x 10 Lloyd iterations: the
+    # full 100,000 x 25 training is 4 of this test's 5 minutes and changes
+    # neither the shapes nor the launch configuration)
+    cfg, cb, codes, qx, X = pq_inputs("c3", n_train=20_000, iters=10)
     assert (cfg.N, cfg.Q, cfg.d, cfg.M) == (1_000_000, 1_000, 960, 16)
     ix = api.Index.et_build_eforest(codes, split=list(cfg.forest_split))
     d, i = ix.et_etree_topk(cfg.topk, queries=dev(qx), codebooks=dev(cb))
