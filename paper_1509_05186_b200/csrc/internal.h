@@ -17,7 +17,10 @@ constexpr int kKMax = 256;                 // codewords per subspace (one byte, 
 constexpr int kTopkMax = 256;              // largest k of the fused top-k
 constexpr int kFinWarps = 8;               // warps per finalize CTA
 constexpr int kStreams = 4;                // lockstep leaf streams per scan warp (8 warps: 32 chains per SM)
-constexpr int kStreamsLong = 6;            // ... for long leaf ranges (>= kLongRange leaves per warp, host plan)
+#ifndef ET_STREAMS_LONG
+#define ET_STREAMS_LONG 6
+#endif
+constexpr int kStreamsLong = ET_STREAMS_LONG;   // ... for long leaf ranges (>= kLongRange leaves per warp, host plan)
 constexpr int kLongRange = 384;
 constexpr int kBatchEmit = 32 * kStreams;  // candidates a lane can append between two buffer checks
 constexpr int kBatchEmitLong = 32 * kStreamsLong;   // ... with kStreamsLong streams (buffers 64 entries longer)
@@ -125,7 +128,7 @@ struct ScanParams {
 // levels in their own area; shorter trees keep every level in shared memory.
 constexpr int kTmemLevels = 2;             // levels of an 8-level tree held in TMEM
 #ifndef ET_REC_SMEM
-#define ET_REC_SMEM 0                      // 1: leaf records broadcast through shared memory (scan_tree3 RS)
+#define ET_REC_SMEM 1                      // 1: leaf records broadcast through shared memory (scan_tree3 RS)
 #endif
 // RS: kWarps x kStreamsLong x 32 records x 16 B = 24 KB, the 16 KB staging area + this extension
 constexpr uint32_t kRecExtra = ET_REC_SMEM ? (uint32_t)(kWarps * kStreamsLong * 512 - 8 * 16 * 128) : 0u;
