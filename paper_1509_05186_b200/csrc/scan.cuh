@@ -1440,6 +1440,7 @@ __device__ void scan_tree3(EmitCtx& e, const SmemScan& sm, const TreeDev& tr, ui
       if constexpr (EX) { cure[k] = nxe[k]; nxe[k] = load_extra(k, off + 32); }
     }
     if constexpr (RS) {
+      ET_CHECK(rs_s + (uint32_t)(NS * 512) <= smem_u32(sm.bigstage) + 8u * 16u * 128u + kRecExtra);
       __syncwarp();                                  // the previous batch's reads are done
 #pragma unroll
       for (int k = 0; k < NS; ++k) sts_u4(rs_s + (uint32_t)(k * 512) + ((uint32_t)lane << 4), cur[k]);
